@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""QSDP communication hot-path benchmark (driver contract: one JSON line).
+
+Metric (BASELINE.json): quantized all-gather + reduce-scatter effective GB/s.
+Workload (configs[1]): GPT-2 small (125M) dense parameter groups, QSDP w8/g8,
+bucket 1024, synthetic N(0, 0.02^2) weights and N(0, 1e-3^2) gradients.  One
+step = one training step's QSDP traffic: for every FSDP group (root + 12
+blocks) a forward all-gather (phase 0), then in reverse order a backward
+re-gather (phase 1) and a gradient reduce-scatter (phase 2) -- the call order
+of forward_layer/backward_layer (pkg/src/qsdp/sharded.py:437-469).
+
+effective GB/s (nccl-tests algbw convention on the fp32 tensor):
+per rank 4*N bytes per collective, 3 collectives per group; ``value`` is the
+whole-job aggregate (sum over ranks), scaling "weak" (each rank dequantizes
+the full model per gather whatever N is).
+
+    python bench.py [--gpus N --steps K --warmup W --model gpt2-125m --wbits 8 --gbits 8 --bucket 1024]
+    python bench.py --impl reference ...   # the reference algorithm on the host CPU (oracle port)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--model", default="gpt2-125m")
+    ap.add_argument("--wbits", type=int, default=8)
+    ap.add_argument("--gbits", type=int, default=8)
+    ap.add_argument("--bucket", type=int, default=1024)
+    ap.add_argument("--out-dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sms = sorted(s[0] for s in self.samples)
+        reasons = set()
+        for _, _, mask in self.samples:
+            for bit, name in REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the reference algorithm (oracle port of pkg/src/qsdp) on host cores.
+# ---------------------------------------------------------------------------
+
+def cpu_protocol_step(O, full_w, grads, P, wbits, gbits, bucket, step, threads):
+    """AG(fwd) + AG(bwd) + RS over P virtual ranks, as sharded.py:323-433."""
+    O.gather(full_w, P, bucket, wbits, 0, step, 1, 0, threads)
+    O.gather(full_w, P, bucket, wbits, 0, step, 1, 1, threads)
+    O.reduce_scatter(grads, bucket, gbits, 0, step, 1, threads)
+
+
+def cpu_sample(model, world):
+    import numpy as np
+    from paper_2302_02390_b200.gpt import dense_groups
+    g = dense_groups(model)[1]  # first transformer block group
+    n = max(1 << 18, g.numel // max(1, world))
+    rng = np.random.default_rng(0)
+    w = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    grads = [(np.random.default_rng(1 + p).standard_normal(n) * 1e-3).astype(np.float32) for p in range(world)]
+    return g, n, w, grads
+
+
+def run_cpu_baseline(args, world, min_seconds=10.0):
+    from oracle import oracle as O
+    threads = len(os.sched_getaffinity(0))
+    _, n, w, grads = cpu_sample(args.model, world)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        cpu_protocol_step(O, w, grads, world, args.wbits, args.gbits, args.bucket, reps, threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or reps >= 50:
+            break
+    value = world * 12.0 * n * reps / el / 1e9
+    return {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{reps} x [AG fwd + AG bwd + RS] of {n} elements (first {args.model} block group, "
+                      f"P={world} virtual ranks), w{args.wbits}/g{args.gbits} bucket {args.bucket}, "
+                      f"{el:.1f} s wall, C oracle (oracle/qsdp_oracle.c) on {threads} threads"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    threads = len(os.sched_getaffinity(0))
+    _, n, w, grads = cpu_sample(args.model, world)
+    for s in range(args.warmup):
+        cpu_protocol_step(O, w, grads, world, args.wbits, args.gbits, args.bucket, s, threads)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        cpu_protocol_step(O, w, grads, world, args.wbits, args.gbits, args.bucket, s, threads)
+    el = time.perf_counter() - t0
+    value = world * 12.0 * n * args.steps / el / 1e9
+    line = {
+        "impl": "reference", "metric": "quantized all-gather+reduce-scatter effective GB/s", "value": round(value, 4),
+        "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.model} QSDP w{args.wbits}/g{args.gbits} bucket {args.bucket}: AG fwd + AG bwd "
+                               f"+ RS, bounded sample of {n} elements per step, P={world} virtual ranks on the host"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{n} elements per step (first block group / P), oracle/qsdp_oracle.c"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_02390_b200 import _lib
+    from paper_2302_02390_b200.comm import QSDPComm, plan_segments
+    from paper_2302_02390_b200.gpt import dense_groups
+    from paper_2302_02390_b200.quantize import (QuantSpec, SegmentKey, codes_bytes, dequant_accumulate,
+                                                dequantize_segments, num_buckets, quantize_segments)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.lib()
+
+    wspec = QuantSpec(args.wbits, args.bucket, "shift")
+    gspec = QuantSpec(args.gbits, args.bucket, "uniform_stochastic")
+    out_dt = torch.float32 if args.out_dtype == "f32" else torch.bfloat16
+    osz = 4 if out_dt == torch.float32 else 2
+    groups = dense_groups(args.model)
+    N_total = sum(g.numel for g in groups)
+    pad = args.bucket if args.bucket % 8 == 0 else 1
+
+    # ---- synthetic state (device-resident for `value`) ----
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    state = []
+    max_seg = 0
+    for gi, g in enumerate(groups):
+        segs = plan_segments(g.numel, world, pad)
+        max_seg = max(max_seg, max(n for _, n in segs))
+        s, n = segs[rank]
+        shard = torch.randn(max(n, 1), generator=gen, device=dev)[:n].mul_(0.02)
+        grad = torch.randn(g.numel, generator=gen, device=dev).mul_(1e-3)
+        full = torch.empty(g.numel, dtype=out_dt, device=dev)
+        gshard = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        wq = (torch.empty(codes_bytes(g.numel, wspec) + 16, dtype=torch.uint8, device=dev),
+              torch.empty((num_buckets(g.numel, args.bucket), 3), dtype=torch.float32, device=dev))
+        gq = (torch.empty(codes_bytes(g.numel, gspec) + 16, dtype=torch.uint8, device=dev),
+              torch.empty((num_buckets(g.numel, args.bucket), 3), dtype=torch.float32, device=dev))
+        state.append(dict(g=g, segs=segs, shard=shard, grad=grad, full=full, gshard=gshard, wq=wq, gq=gq))
+    flush = torch.empty(64 << 20, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
+
+    comm = QSDPComm(max_seg, wspec, gspec, device=dev) if world > 1 or not args.no_e2e else None
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- N=1: batched kernel API with per-kernel CUDA events (same kernels as the comm) ----
+    kinds = ("K1_quantize_shift", "K3_dequantize", "K2_quantize_stochastic", "K4_dequant_accumulate")
+    kbytes = {k: 0 for k in kinds}
+    kev = {k: [] for k in kinds}
+    launches = [0]
+
+    def timed(kind, fn, nbytes, record):
+        if record:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            kev[kind].append((a, b))
+            kbytes[kind] += nbytes
+        else:
+            fn()
+        launches[0] += 1
+
+    def ag_local(st, gi, step, phase, record):
+        n = st["g"].numel
+        res = {}
+
+        def q():
+            res["cm"] = quantize_segments([(st["shard"], 0, SegmentKey(0, step, gi, phase, 0))], wspec,
+                                          out=[st["wq"]])[0]
+        cb = codes_bytes(n, wspec) + 12 * num_buckets(n, args.bucket)
+        timed(kinds[0], q, 4 * n + cb, record)
+        c, m = res["cm"]
+        timed(kinds[1], lambda: dequantize_segments([(c, m, n, st["full"])], wspec, out_dt), cb + osz * n, record)
+
+    def rs_local(st, gi, step, record):
+        n = st["g"].numel
+        res = {}
+
+        def q():
+            res["cm"] = quantize_segments([(st["grad"], 0, SegmentKey(0, step, gi, 2, 0))], gspec,
+                                          out=[st["gq"]])[0]
+        cb = codes_bytes(n, gspec) + 12 * num_buckets(n, args.bucket)
+        timed(kinds[2], q, 4 * n + cb, record)
+        timed(kinds[3], lambda: dequant_accumulate([res["cm"]], n, gspec, 1, dtype=torch.float32,
+                                                   out=st["gshard"]), cb + 4 * n, record)
+
+    def step_local(step, record):
+        for gi, st in enumerate(state):
+            ag_local(st, gi, step, 0, record)
+        for gi in range(len(state) - 1, -1, -1):
+            ag_local(state[gi], gi, step, 1, record)
+            rs_local(state[gi], gi, step, record)
+
+    def step_comm(step):
+        for gi, st in enumerate(state):
+            comm.all_gather(st["shard"], st["segs"], SegmentKey(0, step, gi, 0, 0), st["full"])
+        for gi in range(len(state) - 1, -1, -1):
+            st = state[gi]
+            comm.all_gather(st["shard"], st["segs"], SegmentKey(0, step, gi, 1, 0), st["full"])
+            comm.reduce_scatter(st["grad"], st["segs"], SegmentKey(0, step, gi, 2, rank), st["gshard"])
+        launches[0] += len(state) * 3 * (3 if world > 1 else 2)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    run_step = (lambda s, rec: step_local(s, rec)) if world == 1 else (lambda s, rec: step_comm(s))
+    for s in range(args.warmup):
+        run_step(s, False)
+    barrier()
+    launches[0] = 0
+    step_events = []
+    with ClockSampler(local) as clocks:
+        barrier()
+        for s in range(args.steps):
+            flush.fill_(s)  # evict L2 between timed steps (outside the step events)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run_step(args.warmup + s, True)
+            b.record(stream)
+            step_events.append((a, b))
+        barrier()
+    ms = sum(a.elapsed_time(b) for a, b in step_events)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * 12.0 * N_total / (ms_step * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (N=1: per-kernel events inside the timed region) ----
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    kernels = {}
+    roofline = None
+    if world == 1:
+        for k in kinds:
+            tk = sum(a.elapsed_time(b) for a, b in kev[k])
+            if kev[k]:
+                kernels[k] = {"ms_total": round(tk, 4), "launches": len(kev[k]),
+                              "gbs": round(kbytes[k] / (tk * 1e-3) / 1e9, 1), "share": round(tk / ms, 4)}
+        dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
+        ach = kernels[dom]["gbs"]
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            traffic = tr.get(args.model, {}).get(dom)
+        except Exception:
+            pass
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
+                    "bytes_per_launch": round(kbytes[dom] / len(kev[dom]))}
+
+    # ---- e2e: through the C-ABI communicator, host buffers, copies inside the timed region ----
+    e2e = None
+    if not args.no_e2e and comm is not None:
+        host = []
+        for st in state:
+            host.append(dict(shard=st["shard"].cpu().pin_memory(), grad=st["grad"].cpu().pin_memory(),
+                             res=torch.empty_like(st["gshard"], device="cpu").pin_memory()))
+        bi = sum(h["shard"].numel() * 4 + h["grad"].numel() * 4 for h in host)
+        bo = sum(st["segs"][rank][1] * 4 for st in state)
+
+        def step_e2e(step):
+            for gi, (st, h) in enumerate(zip(state, host)):
+                st["shard"].copy_(h["shard"], non_blocking=True)
+                st["grad"].copy_(h["grad"], non_blocking=True)
+            for gi, st in enumerate(state):
+                comm.all_gather(st["shard"], st["segs"], SegmentKey(0, step, gi, 0, 0), st["full"])
+            for gi in range(len(state) - 1, -1, -1):
+                st = state[gi]
+                comm.all_gather(st["shard"], st["segs"], SegmentKey(0, step, gi, 1, 0), st["full"])
+                comm.reduce_scatter(st["grad"], st["segs"], SegmentKey(0, step, gi, 2, rank), st["gshard"])
+                n = st["segs"][rank][1]
+                host[gi]["res"][:n].copy_(st["gshard"][:n], non_blocking=True)
+
+        for s in range(max(1, args.warmup)):
+            step_e2e(s)
+        barrier()
+        ev = []
+        for s in range(args.steps):
+            flush.fill_(s)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step_e2e(s)
+            b.record(stream)
+            ev.append((a, b))
+        barrier()
+        ems = sum(a.elapsed_time(b) for a, b in ev)
+        if world > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": round(world * 12.0 * N_total / (ems / args.steps * 1e-3) / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "ms_per_step": round(ems / args.steps, 3),
+               "path": "QSDPComm -> qsdp_all_gather / qsdp_reduce_scatter (C ABI), pinned host buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(args, world)
+
+    if rank == 0:
+        line = {
+            "metric": "quantized all-gather+reduce-scatter effective GB/s", "value": round(value, 2),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.model} QSDP w{args.wbits}/g{args.gbits} bucket {args.bucket}: per step "
+                                   f"AG fwd + AG bwd + RS over {len(groups)} FSDP groups ({N_total} dense params)",
+                       "out_dtype": args.out_dtype, "quantizer_input": "f32", "arithmetic": "f64 (bit-exact)",
+                       "l2": "256 MB L2 flush between timed steps; per-step working set > 126 MB L2",
+                       "parallelism": f"qsdp{world}", "convention": "sum over ranks of 4*N per collective / time"},
+            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches[0], "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

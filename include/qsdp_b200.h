@@ -1,0 +1,170 @@
+/*
+ * qsdp_b200.h -- C ABI of the B200-native QSDP communication hot path.
+ *
+ * Drop-in boundary for the reference's quantizer and FSDP-hook API
+ * (reference = arxiv/paper_2302_02390 artifact, pkg/src/qsdp; paths below are
+ * relative to that package).  Every entry point is extern "C", takes plain
+ * device pointers and sizes, and is stream-ordered on the caller's
+ * cudaStream_t (passed as void*) with no hidden device synchronisation.
+ *
+ *   reference (Python/NumPy)                         replaced by
+ *   ------------------------------------------------ ---------------------------------
+ *   quantize_bucket / _segment_blocks (shift)         qsdp_quantize / qsdp_quantize_batch
+ *     quantize.py:235-272, sharded.py:243-248            (inner = QSDP_INNER_SHIFT)
+ *   quantize_bucket (uniform_stochastic | flip)       qsdp_quantize / qsdp_quantize_batch
+ *     quantize.py:273-274, 316-321                       (inner = QSDP_INNER_STOCHASTIC)
+ *   bucket_rng / sample_shift / rng.random            device SeedSequence->PCG64 (no entry point;
+ *     sharded.py:235-240, quantize.py:130-132            keyed by qsdp_key + bucket start)
+ *   _pack_codes / _unpack_codes  wire.py:82-95         packed code layout of every entry point
+ *   dequantize  quantize.py:209-232                    qsdp_dequantize / qsdp_dequantize_batch
+ *   acc = acc + vals ... acc / P  sharded.py:385-431   qsdp_dequant_accumulate
+ *   message_size_bits  wire.py:187-192                 qsdp_message_size_bits
+ *   encode  wire.py:108-131                            qsdp_wire_encode (host export of one segment)
+ *   ShardedMLP._gather  sharded.py:323-373             qsdp_all_gather (one process per GPU)
+ *   ShardedMLP._reduce_scatter  sharded.py:375-433     qsdp_reduce_scatter
+ *
+ * Device layout of one quantized segment (length L, bucket S, width b):
+ *   codes: bucket j's LSB-first packed codes at byte j*ceil(S*b/8), each bucket
+ *          zero-padded to a whole byte (exactly the wire payload, wire.py:14-20);
+ *   meta:  float[nb][3] = {shift, scale_lo, scale_hi} per bucket (the wire's
+ *          per-block field order).
+ *
+ * Error behaviour mirrors the reference exception types:
+ *   QSDP_EINVAL     ValueError for bad arguments (bit width, bucket size, ...)
+ *   QSDP_ENONFINITE ValueError("non-finite ... at index i") -- reported through
+ *                   the optional device word *d_bad (see qsdp_quantize)
+ *   QSDP_ERANGE     CodeRangeError / DecodeError (qsdp_wire_decode)
+ *   QSDP_ECUDA      CUDA runtime failure (message in qsdp_last_error())
+ *   QSDP_EPEER      peer-memory / IPC setup failure
+ */
+#ifndef QSDP_B200_H_
+#define QSDP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QSDP_OK = 0,
+  QSDP_EINVAL = 1,
+  QSDP_ENONFINITE = 2,
+  QSDP_ERANGE = 3,
+  QSDP_ECUDA = 4,
+  QSDP_ENCCL = 5,
+  QSDP_EPEER = 6
+} qsdp_status;
+
+typedef enum { QSDP_INNER_SHIFT = 0, QSDP_INNER_STOCHASTIC = 1 } qsdp_inner;
+typedef enum { QSDP_NOISE_PCG64_SEEDSEQ = 0 } qsdp_noise;
+typedef enum { QSDP_F32 = 0, QSDP_F64 = 1, QSDP_BF16 = 2 } qsdp_dtype;
+
+/* mirrors QuantConfig (sharded.py:76-93) for one tensor class */
+typedef struct {
+  int32_t bits;   /* 1..16 */
+  int32_t bucket; /* >= 1 (BucketSpec.bucket_size, quantize.py:64-75) */
+  int32_t inner;  /* qsdp_inner */
+  int32_t noise;  /* qsdp_noise */
+} qsdp_qcfg;
+
+/* bucket_rng(root_seed, step, layer_idx, phase, worker, start): the bucket start
+   is implicit (segment global_start + j*bucket). */
+typedef struct {
+  uint64_t root_seed, step, layer, phase, worker;
+} qsdp_key;
+
+/* a shard / reduce-scatter segment: buckets are cut from its own start and keyed
+   with start = global_start + j*bucket (sharded.py:243-248, 334-343). */
+typedef struct {
+  int64_t global_start, length;
+} qsdp_segment;
+
+/* One entry of a batched quantize: input segment -> packed codes + meta. */
+typedef struct {
+  const void* x;       /* device, dtype given by the call */
+  qsdp_segment seg;
+  qsdp_key key;
+  uint8_t* codes;      /* device, qsdp_codes_bytes(seg.length, cfg) bytes */
+  float* meta;         /* device, 3*qsdp_num_buckets(seg.length, cfg->bucket) floats */
+} qsdp_qitem;
+
+/* One entry of a batched dequantize / dequant-accumulate. */
+typedef struct {
+  const uint8_t* codes[8]; /* nsrc sources with identical bucket structure */
+  const float* meta[8];
+  int32_t nsrc;
+  int64_t length;
+  void* out;               /* device, dtype given by the call */
+} qsdp_ditem;
+
+#define QSDP_IPC_HANDLE_BYTES 64
+#define QSDP_MAX_WORLD 8
+
+typedef struct qsdp_comm qsdp_comm;
+
+/* ---- sizes & accounting (pure host functions) ---- */
+int64_t qsdp_num_buckets(int64_t length, int32_t bucket);
+int64_t qsdp_codes_bytes(int64_t length, const qsdp_qcfg* cfg);
+/* encoded message size of one segment incl. header/meta/padding (wire.py:187-192) */
+int64_t qsdp_message_size_bits(int64_t length, const qsdp_qcfg* cfg);
+/* shard_bounds(size, P) (sharded.py:193-200): writes P segments */
+void qsdp_shard_bounds(int64_t size, int32_t world, qsdp_segment* out);
+const char* qsdp_last_error(void);
+const char* qsdp_version(void);
+
+/* ---- K1/K2: quantize ----
+ * x: device fp32 or fp64 (x_dtype).  d_bad (optional device uint64, initialise
+ * to UINT64_MAX) receives min over non-finite elements of (item<<40 | index in
+ * segment); buckets containing one are emitted as zero codes / zero meta. */
+qsdp_status qsdp_quantize(const void* x, int32_t x_dtype, qsdp_segment seg, const qsdp_qcfg* cfg,
+                          const qsdp_key* key, uint8_t* codes, float* meta, uint64_t* d_bad,
+                          void* stream);
+qsdp_status qsdp_quantize_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
+                                const qsdp_qcfg* cfg, uint64_t* d_bad, void* stream);
+
+/* ---- K3: dequantize one segment (fp32 out == float32(reference fp64); bf16 == RNE of that) ---- */
+qsdp_status qsdp_dequantize(const uint8_t* codes, const float* meta, int64_t length,
+                            const qsdp_qcfg* cfg, void* out, int32_t out_dtype, void* stream);
+qsdp_status qsdp_dequantize_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
+                                  int32_t out_dtype, void* stream);
+
+/* ---- K4: out = (0 + sum_{p<nsrc} dequant(src_p)) / divisor, fp64 ordered sum ---- */
+qsdp_status qsdp_dequant_accumulate(const uint8_t* const* codes, const float* const* meta,
+                                    int32_t nsrc, int64_t length, const qsdp_qcfg* cfg,
+                                    int32_t divisor, void* out, int32_t out_dtype, void* stream);
+qsdp_status qsdp_dequant_accumulate_batch(const qsdp_ditem* items, int32_t nitems,
+                                          const qsdp_qcfg* cfg, int32_t divisor,
+                                          int32_t out_dtype, void* stream);
+
+/* ---- host wire export (wire.py:108-131): codes/meta already on the host ---- */
+int64_t qsdp_wire_encode(const uint8_t* codes, const float* meta, int64_t length,
+                         const qsdp_qcfg* cfg, uint8_t* out, int64_t out_cap);
+
+/* ---- C1/C2: multi-GPU collectives over NVLink peer memory (one process per GPU) ----
+ * create -> export this rank's IPC handle -> exchange handles out of band
+ * (any transport; the Python host uses torch.distributed) -> open peers. */
+qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32_t device,
+                             int64_t max_segment_elems, const qsdp_qcfg* wcfg,
+                             const qsdp_qcfg* gcfg);
+qsdp_status qsdp_comm_ipc_handle(qsdp_comm* c, void* handle /* QSDP_IPC_HANDLE_BYTES */);
+qsdp_status qsdp_comm_open_peers(qsdp_comm* c, const void* handles /* world*QSDP_IPC_HANDLE_BYTES */);
+/* Quantized all-gather (ShardedMLP._gather): this rank's shard = segs[rank];
+ * every rank writes the dequantized full tensor (sum of segs lengths) to full_out.
+ * key->worker is forced to 0 (sharded.py:341). */
+qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype,
+                            const qsdp_segment* segs, const qsdp_key* key, void* full_out,
+                            int32_t out_dtype, void* stream);
+/* Quantized reduce-scatter (ShardedMLP._reduce_scatter): full_grad holds this
+ * rank's whole gradient; segs[q] is destination q's shard; shard_out receives
+ * (sum_p dequant(Q_p(grad_p[segs[rank]]))) / world.  key->worker = this rank. */
+qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_dtype,
+                                const qsdp_segment* segs, const qsdp_key* key, void* shard_out,
+                                int32_t out_dtype, void* stream);
+qsdp_status qsdp_comm_destroy(qsdp_comm* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSDP_B200_H_ */

@@ -1,0 +1,134 @@
+"""ctypes binding of the C ABI in include/qsdp_b200.h (libqsdp_b200.so).
+
+The product path has no fallback: if the shared library is missing or a CUDA
+device is absent, calls raise instead of computing anything on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqsdp_b200.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+QSDP_OK = 0
+QSDP_EINVAL = 1
+QSDP_ENONFINITE = 2
+QSDP_ERANGE = 3
+QSDP_ECUDA = 4
+QSDP_ENCCL = 5
+QSDP_EPEER = 6
+
+INNER_SHIFT = 0
+INNER_STOCHASTIC = 1
+F32, F64, BF16 = 0, 1, 2
+IPC_HANDLE_BYTES = 64
+MAX_WORLD = 8
+
+EXPORTED_SYMBOLS = (
+    "qsdp_num_buckets", "qsdp_codes_bytes", "qsdp_message_size_bits", "qsdp_shard_bounds",
+    "qsdp_last_error", "qsdp_version", "qsdp_quantize", "qsdp_quantize_batch", "qsdp_dequantize",
+    "qsdp_dequantize_batch", "qsdp_dequant_accumulate", "qsdp_dequant_accumulate_batch",
+    "qsdp_wire_encode", "qsdp_comm_create", "qsdp_comm_ipc_handle", "qsdp_comm_open_peers",
+    "qsdp_all_gather", "qsdp_reduce_scatter", "qsdp_comm_destroy",
+)
+
+
+class QCfg(ctypes.Structure):
+    _fields_ = [("bits", ctypes.c_int32), ("bucket", ctypes.c_int32),
+                ("inner", ctypes.c_int32), ("noise", ctypes.c_int32)]
+
+
+class Key(ctypes.Structure):
+    _fields_ = [("root_seed", ctypes.c_uint64), ("step", ctypes.c_uint64),
+                ("layer", ctypes.c_uint64), ("phase", ctypes.c_uint64),
+                ("worker", ctypes.c_uint64)]
+
+
+class Segment(ctypes.Structure):
+    _fields_ = [("global_start", ctypes.c_int64), ("length", ctypes.c_int64)]
+
+
+class QItem(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_void_p), ("seg", Segment), ("key", Key),
+                ("codes", ctypes.c_void_p), ("meta", ctypes.c_void_p)]
+
+
+class DItem(ctypes.Structure):
+    _fields_ = [("codes", ctypes.c_void_p * 8), ("meta", ctypes.c_void_p * 8),
+                ("nsrc", ctypes.c_int32), ("length", ctypes.c_int64), ("out", ctypes.c_void_p)]
+
+
+class QSDPError(RuntimeError):
+    """CUDA / peer failure inside the native library."""
+
+
+_lib = None
+
+
+def build(jobs: int = 4) -> str:
+    """Compile libqsdp_b200.so for sm_100a (nvcc; no GPU needed)."""
+    subprocess.run(["make", "-s", f"-j{jobs}", "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `make -C {CSRC}` (or __graft_entry__.build()). "
+            "There is no CPU fallback for the QSDP hot path.")
+    L = ctypes.CDLL(LIB_PATH)
+    i64, i32, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+    cfgp = ctypes.POINTER(QCfg)
+    keyp = ctypes.POINTER(Key)
+    segp = ctypes.POINTER(Segment)
+    L.qsdp_num_buckets.argtypes = [i64, i32]
+    L.qsdp_num_buckets.restype = i64
+    L.qsdp_codes_bytes.argtypes = [i64, cfgp]
+    L.qsdp_codes_bytes.restype = i64
+    L.qsdp_message_size_bits.argtypes = [i64, cfgp]
+    L.qsdp_message_size_bits.restype = i64
+    L.qsdp_shard_bounds.argtypes = [i64, i32, segp]
+    L.qsdp_shard_bounds.restype = None
+    L.qsdp_last_error.restype = ctypes.c_char_p
+    L.qsdp_version.restype = ctypes.c_char_p
+    L.qsdp_quantize.argtypes = [vp, i32, Segment, cfgp, keyp, vp, vp, vp, vp]
+    L.qsdp_quantize_batch.argtypes = [ctypes.POINTER(QItem), i32, i32, cfgp, vp, vp]
+    L.qsdp_dequantize.argtypes = [vp, vp, i64, cfgp, vp, i32, vp]
+    L.qsdp_dequantize_batch.argtypes = [ctypes.POINTER(DItem), i32, cfgp, i32, vp]
+    L.qsdp_dequant_accumulate.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i64, cfgp,
+                                          i32, vp, i32, vp]
+    L.qsdp_dequant_accumulate_batch.argtypes = [ctypes.POINTER(DItem), i32, cfgp, i32, i32, vp]
+    L.qsdp_wire_encode.argtypes = [vp, vp, i64, cfgp, vp, i64]
+    L.qsdp_wire_encode.restype = i64
+    L.qsdp_comm_create.argtypes = [ctypes.POINTER(vp), i32, i32, i32, i64, cfgp, cfgp]
+    L.qsdp_comm_ipc_handle.argtypes = [vp, vp]
+    L.qsdp_comm_open_peers.argtypes = [vp, vp]
+    L.qsdp_all_gather.argtypes = [vp, vp, i32, segp, keyp, vp, i32, vp]
+    L.qsdp_reduce_scatter.argtypes = [vp, vp, i32, segp, keyp, vp, i32, vp]
+    L.qsdp_comm_destroy.argtypes = [vp]
+    for name in ("qsdp_quantize", "qsdp_quantize_batch", "qsdp_dequantize", "qsdp_dequantize_batch",
+                 "qsdp_dequant_accumulate", "qsdp_dequant_accumulate_batch", "qsdp_comm_create",
+                 "qsdp_comm_ipc_handle", "qsdp_comm_open_peers", "qsdp_all_gather",
+                 "qsdp_reduce_scatter", "qsdp_comm_destroy"):
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    """Map a qsdp_status to the reference's exception types."""
+    if status == QSDP_OK:
+        return
+    msg = lib().qsdp_last_error().decode(errors="replace")
+    if status in (QSDP_EINVAL, QSDP_ENONFINITE):
+        raise ValueError(msg)
+    if status == QSDP_ERANGE:
+        raise ValueError(msg)
+    raise QSDPError(f"qsdp status {status}: {msg}")

@@ -1,0 +1,124 @@
+"""One-process-per-GPU quantized collectives (C1 all-gather / C2 reduce-scatter).
+
+:class:`QSDPComm` wraps the C-ABI communicator (include/qsdp_b200.h): every
+rank allocates a workspace, exports a CUDA IPC handle, the handles are
+exchanged once over ``torch.distributed`` (host plumbing only), and from then
+on the data path is the library's own kernels reading peers' HBM over NVLink --
+no NCCL call sits on it.
+
+Keys follow the reference protocol (pkg/src/qsdp/sharded.py:323-433):
+all-gather buckets are keyed (root, step, layer, phase, worker=0, start) with
+the shard's global start; reduce-scatter buckets (root, step, layer,
+PHASE_GRAD, worker=rank, start of the destination segment).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .quantize import QuantSpec, SegmentKey, _DTYPE_CODE
+
+__all__ = ["QSDPComm", "plan_segments"]
+
+
+def plan_segments(size: int, world: int, pad_to: int = 1):
+    """Per-rank (global_start, length) segments of a flat tensor.
+
+    ``pad_to == 1`` reproduces ``shard_bounds`` (sharded.py:193-200: remainder
+    to the last rank).  ``pad_to > 1`` gives FSDP2-style equal shards padded to
+    a multiple of ``pad_to`` elements (the last ones may be short or empty).
+    """
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if pad_to <= 1:
+        base = size // world
+        return [(p * base, base if p < world - 1 else size - p * base) for p in range(world)]
+    per = -(-size // world)
+    per = -(-per // pad_to) * pad_to
+    segs = []
+    for p in range(world):
+        s = min(p * per, size)
+        segs.append((s, max(0, min(per, size - s))))
+    return segs
+
+
+class QSDPComm:
+    """NVLink peer-memory communicator for QSDP's quantized AG / RS."""
+
+    def __init__(self, max_segment_elems: int, wspec: QuantSpec, gspec: QuantSpec,
+                 group: dist.ProcessGroup | None = None, device: torch.device | None = None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if self.world > _lib.MAX_WORLD:
+            raise ValueError(f"at most {_lib.MAX_WORLD} ranks per box")
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.wspec, self.gspec = wspec, gspec
+        self.max_segment_elems = int(max_segment_elems)
+        self._wcfg, self._gcfg = wspec.cfg(), gspec.cfg()
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(L.qsdp_comm_create(ctypes.byref(h), self.rank, self.world, self.device.index,
+                                          self.max_segment_elems, ctypes.byref(self._wcfg),
+                                          ctypes.byref(self._gcfg)))
+        self._h = h
+        if self.world > 1:
+            buf = (ctypes.c_uint8 * _lib.IPC_HANDLE_BYTES)()
+            _lib.check(L.qsdp_comm_ipc_handle(self._h, buf))
+            mine = bytes(buf)
+            allh = [None] * self.world
+            dist.all_gather_object(allh, mine, group=group)
+            blob = b"".join(allh)
+            cb = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+            _lib.check(L.qsdp_comm_open_peers(self._h, cb))
+            dist.barrier(group=group)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().qsdp_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _segs(self, segs):
+        if len(segs) != self.world:
+            raise ValueError("need one segment per rank")
+        arr = (_lib.Segment * self.world)()
+        for p, (s, n) in enumerate(segs):
+            arr[p] = _lib.Segment(int(s), int(n))
+        return arr
+
+    def all_gather(self, shard: torch.Tensor, segs, key: SegmentKey, out: torch.Tensor) -> torch.Tensor:
+        """C1: ``out`` (the full tensor, element 0 = segs[0] start) receives every
+        rank's dequantized shard; ``shard`` is this rank's segs[rank] slice."""
+        if shard.numel() != segs[self.rank][1]:
+            raise ValueError("shard length does not match its segment")
+        arr = self._segs(segs)
+        k = key.c()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().qsdp_all_gather(
+                self._h, shard.data_ptr(), _DTYPE_CODE[shard.dtype], arr, ctypes.byref(k), out.data_ptr(),
+                _DTYPE_CODE[out.dtype], torch.cuda.current_stream(self.device).cuda_stream))
+        return out
+
+    def reduce_scatter(self, full_grad: torch.Tensor, segs, key: SegmentKey, out: torch.Tensor) -> torch.Tensor:
+        """C2: ``out`` (this rank's shard) receives the fp64-ordered average of
+        every rank's dequantized contribution to segs[rank]."""
+        if out.numel() < segs[self.rank][1]:
+            raise ValueError("output shorter than this rank's segment")
+        arr = self._segs(segs)
+        k = key.c()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().qsdp_reduce_scatter(
+                self._h, full_grad.data_ptr(), _DTYPE_CODE[full_grad.dtype], arr, ctypes.byref(k),
+                out.data_ptr(), _DTYPE_CODE[out.dtype], torch.cuda.current_stream(self.device).cuda_stream))
+        return out

@@ -1,0 +1,625 @@
+// qsdp_capi.cu -- the extern "C" boundary (include/qsdp_b200.h) and the
+// multi-GPU collectives C1 (quantized all-gather) / C2 (quantized
+// reduce-scatter) over NVLink peer memory.
+//
+// C1 replaces ShardedMLP._gather (pkg/src/qsdp/sharded.py:323-373):
+//   rank r quantizes its own shard (key worker 0) into its local slot; after a
+//   system-scope flag barrier every rank PULLS all P slots straight from the
+//   peers' HBM over NVLink inside the dequantize kernel, writing the full
+//   gathered tensor -- the transfer is fused into the dequant pass.
+// C2 replaces ShardedMLP._reduce_scatter (sharded.py:375-433):
+//   rank r quantizes all P destination segments of its gradient (key worker r)
+//   into P local slots; after the barrier, owner q pulls slot q from sources
+//   p = 0..P-1 in order and dequant-accumulates in fp64, then divides by P.
+// Slots are double-buffered by call parity, so one barrier per collective
+// suffices: a rank rewrites parity k's slots only after every peer has passed
+// the barrier of call k+1, i.e. finished reading call k-1's data.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qsdp_b200.h"
+#include "qsdp_device.cuh"
+
+namespace qsdp {
+cudaError_t launch_quantize_f32(const QJobTable& tab, bool vec, int sms, cudaStream_t s);
+cudaError_t launch_quantize_f64(const QJobTable& tab, bool vec, int sms, cudaStream_t s);
+cudaError_t launch_dequant(const DJobTable& tab, bool vec, int sms, cudaStream_t s);
+cudaError_t upload_jump_f32(const JumpEntry* host);
+cudaError_t upload_jump_f64(const JumpEntry* host);
+}  // namespace qsdp
+
+using namespace qsdp;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+qsdp_status fail(qsdp_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+qsdp_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(QSDP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define QSDP_CUDA(call)                                    \
+  do {                                                     \
+    cudaError_t _e = (call);                               \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);    \
+  } while (0)
+
+// --- per-device state: SM count + jump table uploaded once -----------------
+struct DeviceState {
+  int sms = 0;
+  bool jump_ready = false;
+};
+std::mutex g_mu;
+DeviceState g_dev[64];
+
+qsdp_status ensure_device(int& sms) {
+  int dev = 0;
+  QSDP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  DeviceState& d = g_dev[dev & 63];
+  if (!d.jump_ready) {
+    JumpEntry tab[kJumpTable];
+    U128 a{1, 0}, g{0, 0};
+    const U128 one{1, 0};
+    for (int k = 0; k < kJumpTable; ++k) {
+      tab[k].a = a;
+      tab[k].g = g;
+      g = add128(mul128(pcg_mult(), g), one);  // G_{k+1} = M G_k + 1
+      a = mul128(pcg_mult(), a);               // A_{k+1} = M A_k
+    }
+    QSDP_CUDA(upload_jump_f32(tab));
+    QSDP_CUDA(upload_jump_f64(tab));
+    QSDP_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    d.jump_ready = true;
+  }
+  sms = d.sms;
+  return QSDP_OK;
+}
+
+// SeedSequence prefix: absorb root, step, layer, phase, worker (each coerced to
+// LE uint32 words, 0 -> [0]) -- numpy mix_entropy with pool size 4.
+SeedPrefix make_prefix(const qsdp_key& k, uint64_t worker) {
+  uint32_t words[10];
+  int n = 0;
+  const uint64_t f[5] = {k.root_seed, k.step, k.layer, k.phase, worker};
+  for (uint64_t v : f) {
+    words[n++] = (uint32_t)v;
+    if (v >> 32) words[n++] = (uint32_t)(v >> 32);
+  }
+  SeedPrefix p{};
+  uint32_t hc = SS_INIT_A;
+  for (int i = 0; i < 4; ++i) p.pool[i] = ss_hashmix(words[i], hc);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) p.pool[d] = ss_mix(p.pool[d], ss_hashmix(p.pool[s], hc));
+  for (int s = 4; s < n; ++s) ss_absorb(p.pool, hc, words[s]);
+  p.hash_const = hc;
+  return p;
+}
+
+qsdp_status check_cfg(const qsdp_qcfg* c) {
+  if (c == nullptr) return fail(QSDP_EINVAL, "null qsdp_qcfg");
+  if (c->bits < 1 || c->bits > 16) return fail(QSDP_EINVAL, "bit_width must be in [1, 16]");
+  if (c->bucket < 1) return fail(QSDP_EINVAL, "bucket_size must be >= 1");
+  if (c->inner != QSDP_INNER_SHIFT && c->inner != QSDP_INNER_STOCHASTIC)
+    return fail(QSDP_EINVAL, "unknown inner mode");
+  if (c->noise != QSDP_NOISE_PCG64_SEEDSEQ) return fail(QSDP_EINVAL, "unsupported noise mode");
+  return QSDP_OK;
+}
+
+bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+size_t dtype_size(int dt) { return dt == QSDP_F64 ? 8 : (dt == QSDP_BF16 ? 2 : 4); }
+
+// Split a list of quantize jobs into launches of <= kMaxJobs.
+struct QJobSpec {
+  const void* x;
+  int64_t length, global_start;
+  uint8_t* codes;
+  float* meta;
+  SeedPrefix seed;
+};
+
+qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const qsdp_qcfg* cfg,
+                         uint64_t* d_bad, cudaStream_t stream) {
+  if (x_dtype != QSDP_F32 && x_dtype != QSDP_F64) return fail(QSDP_EINVAL, "input dtype must be f32 or f64");
+  int sms = 0;
+  qsdp_status st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  const size_t esz = dtype_size(x_dtype);
+  size_t i = 0;
+  while (i < jobs.size()) {
+    QJobTable tab;
+    memset(&tab, 0, sizeof(tab));
+    tab.bits = cfg->bits;
+    tab.bucket = cfg->bucket;
+    tab.inner = cfg->inner;
+    tab.bad_index = reinterpret_cast<unsigned long long*>(d_bad);
+    int64_t nb = 0;
+    bool vec = cfg->bucket % 4 == 0;
+    int nj = 0;
+    for (; i < jobs.size() && nj < kMaxJobs; ++i) {
+      const QJobSpec& s = jobs[i];
+      if (s.length <= 0) continue;
+      QJob& J = tab.jobs[nj++];
+      J.x = s.x;
+      J.codes[0] = s.codes;
+      J.meta[0] = s.meta;
+      J.ndst = 1;
+      J.length = s.length;
+      J.global_start = s.global_start;
+      J.bucket_base = nb;
+      J.seed = s.seed;
+      nb += (s.length + cfg->bucket - 1) / cfg->bucket;
+      vec = vec && aligned(s.x, 16);
+      (void)esz;
+    }
+    tab.njobs = nj;
+    tab.total_buckets = nb;
+    if (nj == 0) continue;
+    cudaError_t e = x_dtype == QSDP_F64 ? launch_quantize_f64(tab, vec, sms, stream)
+                                         : launch_quantize_f32(tab, vec, sms, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "quantize kernel launch");
+  }
+  return QSDP_OK;
+}
+
+struct DJobSpec {
+  const uint8_t* codes[8];
+  const float* meta[8];
+  int nsrc;
+  int64_t length;
+  void* out;
+};
+
+qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg, int accumulate,
+                        int divisor, int out_dtype, cudaStream_t stream) {
+  if (out_dtype != QSDP_F32 && out_dtype != QSDP_F64 && out_dtype != QSDP_BF16)
+    return fail(QSDP_EINVAL, "output dtype must be f32, f64 or bf16");
+  int sms = 0;
+  qsdp_status st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  size_t i = 0;
+  while (i < jobs.size()) {
+    DJobTable tab;
+    memset(&tab, 0, sizeof(tab));
+    tab.bits = cfg->bits;
+    tab.bucket = cfg->bucket;
+    tab.out_dtype = out_dtype;
+    tab.accumulate = accumulate;
+    tab.divisor = divisor < 1 ? 1 : divisor;
+    bool vec = cfg->bucket % 4 == 0;
+    bool cvec = cfg->bucket % 8 == 0;
+    int64_t nb = 0;
+    int nj = 0;
+    for (; i < jobs.size() && nj < kMaxJobs; ++i) {
+      const DJobSpec& s = jobs[i];
+      if (s.length <= 0) continue;
+      if (s.nsrc < 1 || s.nsrc > 8) return fail(QSDP_EINVAL, "nsrc must be in [1, 8]");
+      DJob& J = tab.jobs[nj++];
+      for (int p = 0; p < s.nsrc; ++p) {
+        J.codes[p] = s.codes[p];
+        J.meta[p] = s.meta[p];
+        cvec = cvec && aligned(s.codes[p], 8);
+      }
+      J.nsrc = s.nsrc;
+      J.out = s.out;
+      J.length = s.length;
+      J.bucket_base = nb;
+      nb += (s.length + cfg->bucket - 1) / cfg->bucket;
+      vec = vec && aligned(s.out, out_dtype == QSDP_BF16 ? 8 : 16);
+    }
+    tab.njobs = nj;
+    tab.total_buckets = nb;
+    tab.codes_vec = cvec ? 1 : 0;
+    if (nj == 0) continue;
+    cudaError_t e = launch_dequant(tab, vec, sms, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dequantize kernel launch");
+  }
+  return QSDP_OK;
+}
+
+int64_t payload(int64_t len, int bits) { return (len * bits + 7) / 8; }
+
+}  // namespace
+
+// ===========================================================================
+// extern "C" entry points
+// ===========================================================================
+extern "C" {
+
+const char* qsdp_last_error(void) { return g_last_error.c_str(); }
+const char* qsdp_version(void) { return "qsdp_b200 0.1 (sm_100a)"; }
+
+int64_t qsdp_num_buckets(int64_t length, int32_t bucket) {
+  if (length <= 0 || bucket < 1) return 0;
+  return (length + bucket - 1) / bucket;
+}
+
+int64_t qsdp_codes_bytes(int64_t length, const qsdp_qcfg* cfg) {
+  if (length <= 0 || cfg == nullptr || cfg->bucket < 1) return 0;
+  const int64_t nb = qsdp_num_buckets(length, cfg->bucket);
+  return (nb - 1) * payload(cfg->bucket, cfg->bits) + payload(length - (nb - 1) * cfg->bucket, cfg->bits);
+}
+
+int64_t qsdp_message_size_bits(int64_t length, const qsdp_qcfg* cfg) {
+  // HEADER_BITS + sum(BLOCK_META_BITS + 8*payload) (wire.py:47-51, 187-192)
+  int64_t bits = 14 * 8;
+  if (length <= 0) return bits;
+  return bits + 96 * qsdp_num_buckets(length, cfg->bucket) + 8 * qsdp_codes_bytes(length, cfg);
+}
+
+void qsdp_shard_bounds(int64_t size, int32_t world, qsdp_segment* out) {
+  const int64_t base = world > 0 ? size / world : 0;
+  for (int p = 0; p < world; ++p) {
+    out[p].global_start = p * base;
+    out[p].length = (p == world - 1) ? size - p * base : base;
+  }
+}
+
+qsdp_status qsdp_quantize(const void* x, int32_t x_dtype, qsdp_segment seg, const qsdp_qcfg* cfg,
+                          const qsdp_key* key, uint8_t* codes, float* meta, uint64_t* d_bad, void* stream) {
+  qsdp_qitem it;
+  it.x = x;
+  it.seg = seg;
+  it.key = *key;
+  it.codes = codes;
+  it.meta = meta;
+  return qsdp_quantize_batch(&it, 1, x_dtype, cfg, d_bad, stream);
+}
+
+qsdp_status qsdp_quantize_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
+                                const qsdp_qcfg* cfg, uint64_t* d_bad, void* stream) {
+  qsdp_status st = check_cfg(cfg);
+  if (st != QSDP_OK) return st;
+  if (nitems < 0 || (nitems > 0 && items == nullptr)) return fail(QSDP_EINVAL, "bad item list");
+  std::vector<QJobSpec> jobs;
+  jobs.reserve(nitems);
+  for (int i = 0; i < nitems; ++i) {
+    const qsdp_qitem& it = items[i];
+    if (it.seg.length < 0 || it.seg.global_start < 0) return fail(QSDP_EINVAL, "negative segment");
+    if (it.seg.length > 0 && (it.x == nullptr || it.codes == nullptr || it.meta == nullptr))
+      return fail(QSDP_EINVAL, "null buffer");
+    const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
+    if (direct && it.seg.length > 0 && !aligned(it.codes, 8))
+      return fail(QSDP_EINVAL, "codes buffer must be 8-byte aligned");
+    QJobSpec s;
+    s.x = it.x;
+    s.length = it.seg.length;
+    s.global_start = it.seg.global_start;
+    s.codes = it.codes;
+    s.meta = it.meta;
+    s.seed = make_prefix(it.key, it.key.worker);
+    jobs.push_back(s);
+  }
+  return run_quantize(jobs, x_dtype, cfg, d_bad, reinterpret_cast<cudaStream_t>(stream));
+}
+
+qsdp_status qsdp_dequantize(const uint8_t* codes, const float* meta, int64_t length, const qsdp_qcfg* cfg,
+                            void* out, int32_t out_dtype, void* stream) {
+  qsdp_ditem it;
+  memset(&it, 0, sizeof(it));
+  it.codes[0] = codes;
+  it.meta[0] = meta;
+  it.nsrc = 1;
+  it.length = length;
+  it.out = out;
+  return qsdp_dequantize_batch(&it, 1, cfg, out_dtype, stream);
+}
+
+static qsdp_status dequant_items(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg, int acc,
+                                 int32_t divisor, int32_t out_dtype, void* stream) {
+  qsdp_status st = check_cfg(cfg);
+  if (st != QSDP_OK) return st;
+  std::vector<DJobSpec> jobs;
+  jobs.reserve(nitems);
+  for (int i = 0; i < nitems; ++i) {
+    const qsdp_ditem& it = items[i];
+    if (it.length < 0) return fail(QSDP_EINVAL, "negative length");
+    if (it.nsrc < 1 || it.nsrc > 8) return fail(QSDP_EINVAL, "nsrc must be in [1, 8]");
+    DJobSpec s;
+    memset(&s, 0, sizeof(s));
+    for (int p = 0; p < it.nsrc; ++p) {
+      s.codes[p] = it.codes[p];
+      s.meta[p] = it.meta[p];
+    }
+    s.nsrc = acc ? it.nsrc : 1;
+    s.length = it.length;
+    s.out = it.out;
+    jobs.push_back(s);
+  }
+  return run_dequant(jobs, cfg, acc, divisor, out_dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+qsdp_status qsdp_dequantize_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
+                                  int32_t out_dtype, void* stream) {
+  return dequant_items(items, nitems, cfg, 0, 1, out_dtype, stream);
+}
+
+qsdp_status qsdp_dequant_accumulate(const uint8_t* const* codes, const float* const* meta, int32_t nsrc,
+                                    int64_t length, const qsdp_qcfg* cfg, int32_t divisor, void* out,
+                                    int32_t out_dtype, void* stream) {
+  if (nsrc < 1 || nsrc > 8) return fail(QSDP_EINVAL, "nsrc must be in [1, 8]");
+  qsdp_ditem it;
+  memset(&it, 0, sizeof(it));
+  for (int p = 0; p < nsrc; ++p) {
+    it.codes[p] = codes[p];
+    it.meta[p] = meta[p];
+  }
+  it.nsrc = nsrc;
+  it.length = length;
+  it.out = out;
+  return dequant_items(&it, 1, cfg, 1, divisor, out_dtype, stream);
+}
+
+qsdp_status qsdp_dequant_accumulate_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
+                                          int32_t divisor, int32_t out_dtype, void* stream) {
+  return dequant_items(items, nitems, cfg, 1, divisor, out_dtype, stream);
+}
+
+int64_t qsdp_wire_encode(const uint8_t* codes, const float* meta, int64_t length, const qsdp_qcfg* cfg,
+                         uint8_t* out, int64_t out_cap) {
+  const int64_t need = qsdp_message_size_bits(length, cfg) / 8;
+  if (out_cap < need) {
+    g_last_error = "wire buffer too small";
+    return -1;
+  }
+  auto put_u32 = [](uint8_t* p, uint32_t v) { memcpy(p, &v, 4); };
+  memset(out, 0, 14);
+  out[0] = 1;  // WIRE_VERSION
+  if (length <= 0) return 14;
+  const int64_t nb = qsdp_num_buckets(length, cfg->bucket);
+  const int64_t pbs = payload(cfg->bucket, cfg->bits);
+  out[1] = (uint8_t)cfg->bits;
+  put_u32(out + 2, (uint32_t)(nb == 1 ? length : cfg->bucket));  // blocks[0].length
+  put_u32(out + 6, (uint32_t)nb);
+  put_u32(out + 10, (uint32_t)length);
+  int64_t o = 14;
+  for (int64_t j = 0; j < nb; ++j) {
+    const int64_t n = length - j * cfg->bucket < cfg->bucket ? length - j * cfg->bucket : cfg->bucket;
+    memcpy(out + o, meta + 3 * j, 12);
+    o += 12;
+    const int64_t pb = payload(n, cfg->bits);
+    memcpy(out + o, codes + j * pbs, (size_t)pb);
+    o += pb;
+  }
+  return o;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Multi-GPU communicator (C1 / C2)
+// ===========================================================================
+struct PeerFlags {
+  unsigned long long* flags[QSDP_MAX_WORLD];  // flags[j] = base of rank j's flag array
+};
+
+__global__ void qsdp_barrier_kernel(PeerFlags pf, int rank, int world, unsigned long long epoch) {
+  const int t = threadIdx.x;
+  if (t < world) {
+    __threadfence_system();
+    unsigned long long* dst = pf.flags[t] + rank;  // peer t learns "rank reached epoch"
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
+    const unsigned long long* mine = pf.flags[rank] + t;
+    unsigned long long v = 0;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+    } while (v < epoch);
+  }
+  __syncthreads();
+}
+
+struct qsdp_comm {
+  int rank = 0, world = 1, device = 0;
+  int64_t max_seg = 0;
+  qsdp_qcfg w{}, g{};
+  size_t slot_codes = 0, slot_meta = 0, slot_bytes = 0;
+  size_t bytes = 0;
+  uint8_t* base = nullptr;
+  uint8_t* peer[QSDP_MAX_WORLD] = {};
+  bool opened[QSDP_MAX_WORLD] = {};
+  unsigned long long epoch = 0;
+
+  static constexpr size_t kFlagBytes = 256;
+  uint8_t* slot(uint8_t* b, int parity, int idx) const {
+    return b + kFlagBytes + ((size_t)parity * world + idx) * slot_bytes;
+  }
+};
+
+static size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+extern "C" {
+
+qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32_t device,
+                             int64_t max_segment_elems, const qsdp_qcfg* wcfg, const qsdp_qcfg* gcfg) {
+  if (out == nullptr) return fail(QSDP_EINVAL, "null out");
+  if (world < 1 || world > QSDP_MAX_WORLD || rank < 0 || rank >= world)
+    return fail(QSDP_EINVAL, "world must be in [1, 8] and 0 <= rank < world");
+  qsdp_status st = check_cfg(wcfg);
+  if (st != QSDP_OK) return st;
+  st = check_cfg(gcfg);
+  if (st != QSDP_OK) return st;
+  QSDP_CUDA(cudaSetDevice(device));
+  int sms = 0;
+  st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  qsdp_comm* c = new qsdp_comm();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->max_seg = max_segment_elems;
+  c->w = *wcfg;
+  c->g = *gcfg;
+  const int64_t cw = qsdp_codes_bytes(max_segment_elems, wcfg), cg = qsdp_codes_bytes(max_segment_elems, gcfg);
+  const int64_t nbw = qsdp_num_buckets(max_segment_elems, wcfg->bucket);
+  const int64_t nbg = qsdp_num_buckets(max_segment_elems, gcfg->bucket);
+  c->slot_codes = round_up((size_t)(cw > cg ? cw : cg) + 16, 256);
+  c->slot_meta = round_up((size_t)(nbw > nbg ? nbw : nbg) * 12 + 16, 256);
+  c->slot_bytes = c->slot_codes + c->slot_meta;
+  c->bytes = qsdp_comm::kFlagBytes + 2 * (size_t)world * c->slot_bytes;
+  cudaError_t e = cudaMalloc(&c->base, c->bytes);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(comm workspace)");
+  }
+  e = cudaMemset(c->base, 0, c->bytes);
+  if (e != cudaSuccess) {
+    cudaFree(c->base);
+    delete c;
+    return cuda_fail(e, "cudaMemset(comm workspace)");
+  }
+  c->peer[rank] = c->base;
+  c->opened[rank] = false;
+  *out = c;
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_comm_ipc_handle(qsdp_comm* c, void* handle) {
+  if (c == nullptr || handle == nullptr) return fail(QSDP_EINVAL, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) <= QSDP_IPC_HANDLE_BYTES, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  QSDP_CUDA(cudaSetDevice(c->device));
+  QSDP_CUDA(cudaIpcGetMemHandle(&h, c->base));
+  memset(handle, 0, QSDP_IPC_HANDLE_BYTES);
+  memcpy(handle, &h, sizeof(h));
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_comm_open_peers(qsdp_comm* c, const void* handles) {
+  if (c == nullptr || handles == nullptr) return fail(QSDP_EINVAL, "null argument");
+  QSDP_CUDA(cudaSetDevice(c->device));
+  for (int j = 0; j < c->world; ++j) {
+    if (j == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)j * QSDP_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(QSDP_EPEER, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    c->peer[j] = static_cast<uint8_t*>(p);
+    c->opened[j] = true;
+  }
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_comm_destroy(qsdp_comm* c) {
+  if (c == nullptr) return QSDP_OK;
+  cudaSetDevice(c->device);
+  for (int j = 0; j < c->world; ++j)
+    if (c->opened[j]) cudaIpcCloseMemHandle(c->peer[j]);
+  if (c->base) cudaFree(c->base);
+  delete c;
+  return QSDP_OK;
+}
+
+static qsdp_status comm_barrier(qsdp_comm* c, cudaStream_t s) {
+  if (c->world == 1) return QSDP_OK;
+  PeerFlags pf;
+  memset(&pf, 0, sizeof(pf));
+  for (int j = 0; j < c->world; ++j) {
+    if (c->peer[j] == nullptr) return fail(QSDP_EPEER, "peers not opened");
+    pf.flags[j] = reinterpret_cast<unsigned long long*>(c->peer[j]);
+  }
+  qsdp_barrier_kernel<<<1, 32, 0, s>>>(pf, c->rank, c->world, c->epoch);
+  QSDP_CUDA(cudaGetLastError());
+  return QSDP_OK;
+}
+
+static qsdp_status check_segs(const qsdp_comm* c, const qsdp_segment* segs) {
+  if (segs == nullptr) return fail(QSDP_EINVAL, "null segments");
+  for (int p = 0; p < c->world; ++p) {
+    if (segs[p].length < 0 || segs[p].length > c->max_seg)
+      return fail(QSDP_EINVAL, "segment longer than the communicator's max_segment_elems");
+    if (segs[p].global_start < segs[0].global_start) return fail(QSDP_EINVAL, "segments must start at segs[0]");
+  }
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, const qsdp_segment* segs,
+                            const qsdp_key* key, void* full_out, int32_t out_dtype, void* stream) {
+  if (c == nullptr || key == nullptr) return fail(QSDP_EINVAL, "null argument");
+  qsdp_status st = check_segs(c, segs);
+  if (st != QSDP_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const qsdp_qcfg* cfg = &c->w;
+  c->epoch += 1;
+  const int par = (int)(c->epoch & 1);
+  // 1. quantize this rank's shard into its local slot (key worker 0, sharded.py:341)
+  std::vector<QJobSpec> q(1);
+  q[0].x = shard;
+  q[0].length = segs[c->rank].length;
+  q[0].global_start = segs[c->rank].global_start;
+  q[0].codes = c->slot(c->base, par, 0);
+  q[0].meta = reinterpret_cast<float*>(c->slot(c->base, par, 0) + c->slot_codes);
+  q[0].seed = make_prefix(*key, 0);
+  st = run_quantize(q, in_dtype, cfg, nullptr, s);
+  if (st != QSDP_OK) return st;
+  // 2. publish + wait for every peer's slot of this call
+  st = comm_barrier(c, s);
+  if (st != QSDP_OK) return st;
+  // 3. pull-dequantize all P shards over NVLink into the gathered buffer
+  std::vector<DJobSpec> d(c->world);
+  const size_t osz = dtype_size(out_dtype);
+  for (int p = 0; p < c->world; ++p) {
+    memset(&d[p], 0, sizeof(DJobSpec));
+    uint8_t* sl = c->slot(c->peer[p], par, 0);
+    d[p].codes[0] = sl;
+    d[p].meta[0] = reinterpret_cast<const float*>(sl + c->slot_codes);
+    d[p].nsrc = 1;
+    d[p].length = segs[p].length;
+    d[p].out = static_cast<uint8_t*>(full_out) + (size_t)(segs[p].global_start - segs[0].global_start) * osz;
+  }
+  return run_dequant(d, cfg, 0, 1, out_dtype, s);
+}
+
+qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_dtype, const qsdp_segment* segs,
+                                const qsdp_key* key, void* shard_out, int32_t out_dtype, void* stream) {
+  if (c == nullptr || key == nullptr) return fail(QSDP_EINVAL, "null argument");
+  qsdp_status st = check_segs(c, segs);
+  if (st != QSDP_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const qsdp_qcfg* cfg = &c->g;
+  c->epoch += 1;
+  const int par = (int)(c->epoch & 1);
+  const size_t isz = dtype_size(in_dtype);
+  // 1. quantize every destination segment of this rank's gradient (worker = rank)
+  const SeedPrefix pre = make_prefix(*key, (uint64_t)c->rank);
+  std::vector<QJobSpec> q(c->world);
+  for (int p = 0; p < c->world; ++p) {
+    q[p].x = static_cast<const uint8_t*>(full_grad) + (size_t)(segs[p].global_start - segs[0].global_start) * isz;
+    q[p].length = segs[p].length;
+    q[p].global_start = segs[p].global_start;
+    q[p].codes = c->slot(c->base, par, p);
+    q[p].meta = reinterpret_cast<float*>(c->slot(c->base, par, p) + c->slot_codes);
+    q[p].seed = pre;
+  }
+  st = run_quantize(q, in_dtype, cfg, nullptr, s);
+  if (st != QSDP_OK) return st;
+  st = comm_barrier(c, s);
+  if (st != QSDP_OK) return st;
+  // 3. owner pulls its segment from sources 0..P-1 (in order) and accumulates
+  std::vector<DJobSpec> d(1);
+  memset(&d[0], 0, sizeof(DJobSpec));
+  for (int p = 0; p < c->world; ++p) {
+    uint8_t* sl = c->slot(c->peer[p], par, c->rank);
+    d[0].codes[p] = sl;
+    d[0].meta[p] = reinterpret_cast<const float*>(sl + c->slot_codes);
+  }
+  d[0].nsrc = c->world;
+  d[0].length = segs[c->rank].length;
+  d[0].out = shard_out;
+  return run_dequant(d, cfg, 1, c->world, out_dtype, s);
+}
+
+}  // extern "C"

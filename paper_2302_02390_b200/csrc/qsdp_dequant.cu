@@ -1,0 +1,40 @@
+// K3 (dequantize) / K4 (ordered dequantize-accumulate) instantiations.
+#include "qsdp_kernels.cuh"
+
+namespace qsdp {
+template <int TL, int OUT, bool ACC>
+static cudaError_t launch_d_tl(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  const int grid = grid_for(tab.total_buckets, 32 / TL, sms);
+  if (vec) dequant_kernel<TL, OUT, true, ACC><<<grid, 256, 0, s>>>(tab);
+  else dequant_kernel<TL, OUT, false, ACC><<<grid, 256, 0, s>>>(tab);
+  return cudaGetLastError();
+}
+
+template <int OUT, bool ACC>
+static cudaError_t launch_d_out(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  int tl = team_lanes(tab.bucket);
+  if (ACC && tl < 8) tl = 8;  // per-source scale rows are filled by lanes 0..nsrc-1
+  switch (tl) {
+    case 1: return launch_d_tl<1, OUT, ACC>(tab, vec, sms, s);
+    case 2: return launch_d_tl<2, OUT, ACC>(tab, vec, sms, s);
+    case 4: return launch_d_tl<4, OUT, ACC>(tab, vec, sms, s);
+    case 8: return launch_d_tl<8, OUT, ACC>(tab, vec, sms, s);
+    case 16: return launch_d_tl<16, OUT, ACC>(tab, vec, sms, s);
+    default: return launch_d_tl<32, OUT, ACC>(tab, vec, sms, s);
+  }
+}
+
+template <bool ACC>
+static cudaError_t launch_d_acc(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  switch (tab.out_dtype) {
+    case 0: return launch_d_out<0, ACC>(tab, vec, sms, s);
+    case 1: return launch_d_out<1, ACC>(tab, vec, sms, s);
+    default: return launch_d_out<2, ACC>(tab, vec, sms, s);
+  }
+}
+
+cudaError_t launch_dequant(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  if (tab.total_buckets == 0) return cudaSuccess;
+  return tab.accumulate ? launch_d_acc<true>(tab, vec, sms, s) : launch_d_acc<false>(tab, vec, sms, s);
+}
+}  // namespace qsdp

@@ -1,0 +1,215 @@
+// qsdp_device.cuh -- device-side building blocks shared by the sm_100a kernels.
+//
+//  * numpy SeedSequence -> PCG64 restated on the device, keyed exactly like the
+//    reference's bucket_rng (pkg/src/qsdp/sharded.py:235-240).  The four
+//    prefix key fields (root_seed, step, layer, phase) plus the worker field
+//    are absorbed on the host once per segment (SeedPrefix); the device absorbs
+//    only the per-bucket `start` word(s) and runs generate_state + PCG64 seeding.
+//  * 128-bit LCG arithmetic for PCG64 stepping and O(1) jump-ahead:
+//    state_{k} = A_k * state_0 + G_k * inc  (mod 2^128).
+//  * the job tables the batched kernels take as __grid_constant__ parameters.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qsdp {
+
+// ---------------------------------------------------------------------------
+// SeedSequence constants (numpy/random/bit_generator.pyx).
+// ---------------------------------------------------------------------------
+constexpr uint32_t SS_INIT_A = 0x43b0d7e5u;
+constexpr uint32_t SS_MULT_A = 0x931e8875u;
+constexpr uint32_t SS_INIT_B = 0x8b51f9ddu;
+constexpr uint32_t SS_MULT_B = 0x58f38dedu;
+constexpr uint32_t SS_MIX_L = 0xca01f9ddu;
+constexpr uint32_t SS_MIX_R = 0x4973f715u;
+
+constexpr uint64_t PCG_MULT_HI = 0x2360ED051FC65DA4ull;
+constexpr uint64_t PCG_MULT_LO = 0x4385DF649FCCF645ull;
+
+// Pool state after absorbing the segment-constant key words.
+struct SeedPrefix {
+  uint32_t pool[4];
+  uint32_t hash_const;
+  uint32_t _pad;
+};
+
+struct U128 {
+  uint64_t lo, hi;
+};
+
+__host__ __device__ __forceinline__ uint32_t ss_hashmix(uint32_t v, uint32_t& hc) {
+  v ^= hc;
+  hc *= SS_MULT_A;
+  v *= hc;
+  v ^= v >> 16;
+  return v;
+}
+__host__ __device__ __forceinline__ uint32_t ss_mix(uint32_t x, uint32_t y) {
+  uint32_t r = SS_MIX_L * x - SS_MIX_R * y;
+  r ^= r >> 16;
+  return r;
+}
+
+__host__ __device__ __forceinline__ void ss_absorb(uint32_t pool[4], uint32_t& hc, uint32_t w) {
+#pragma unroll
+  for (int d = 0; d < 4; ++d) pool[d] = ss_mix(pool[d], ss_hashmix(w, hc));
+}
+
+// Absorb an integer key field (_int_to_uint32_array: LE 32-bit chunks, 0 -> [0]).
+__host__ __device__ __forceinline__ void ss_absorb_u64(uint32_t pool[4], uint32_t& hc, uint64_t v) {
+  ss_absorb(pool, hc, (uint32_t)v);
+  if (v >> 32) ss_absorb(pool, hc, (uint32_t)(v >> 32));
+}
+
+// generate_state(4, uint64) -> v[0..3]; then PCG64 seeding
+// (pcg_setseq_128_srandom_r): inc = (seq<<1)|1, state = (inc+init)*M + inc.
+__host__ __device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+__host__ __device__ __forceinline__ U128 mul128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = mulhi64(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+  return r;
+}
+__host__ __device__ __forceinline__ U128 add128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+  return r;
+}
+// a*b + c (mod 2^128)
+__host__ __device__ __forceinline__ U128 mad128(U128 a, U128 b, U128 c) { return add128(mul128(a, b), c); }
+
+__host__ __device__ __forceinline__ U128 pcg_mult() { return U128{PCG_MULT_LO, PCG_MULT_HI}; }
+
+// Finish SeedSequence for one bucket and seed PCG64; returns (state, inc).
+__host__ __device__ __forceinline__ void seed_bucket(const SeedPrefix& pre, uint64_t start, U128& state,
+                                                     U128& inc) {
+  uint32_t pool[4] = {pre.pool[0], pre.pool[1], pre.pool[2], pre.pool[3]};
+  uint32_t hc = pre.hash_const;
+  ss_absorb_u64(pool, hc, start);
+  uint32_t st[8];
+  uint32_t hb = SS_INIT_B;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i & 3];
+    v ^= hb;
+    hb *= SS_MULT_B;
+    v *= hb;
+    v ^= v >> 16;
+    st[i] = v;
+  }
+  const uint64_t v0 = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
+  const uint64_t v1 = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+  const uint64_t v2 = (uint64_t)st[4] | ((uint64_t)st[5] << 32);
+  const uint64_t v3 = (uint64_t)st[6] | ((uint64_t)st[7] << 32);
+  const U128 init{v1, v0};
+  inc.lo = (v3 << 1) | 1ull;
+  inc.hi = (v2 << 1) | (v3 >> 63);
+  state = mad128(add128(inc, init), pcg_mult(), inc);
+}
+
+// One PCG64 step (state <- state*M + inc) and XSL-RR output of the new state.
+__host__ __device__ __forceinline__ uint64_t pcg_output(U128 s) {
+  const uint64_t x = s.hi ^ s.lo;
+  const unsigned rot = (unsigned)(s.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+// High 32 bits of the XSL-RR output only (one funnel shift instead of two).
+__device__ __forceinline__ uint32_t pcg_output_hi32(U128 s) {
+  const uint64_t x = s.hi ^ s.lo;
+  const unsigned rot = (unsigned)(s.hi >> 58);
+  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+  // rotr64(x, rot) >> 32 == funnel of (xh:xl) by rot, taking the high word.
+  // bits [rot+32, rot+64) of the 128-bit word (x:x).
+  const uint32_t lo_w = rot < 32 ? xh : xl;
+  const uint32_t hi_w = rot < 32 ? xl : xh;
+  return __funnelshift_r(lo_w, hi_w, rot & 31);
+}
+
+// numpy next_double: (x >> 11) * 2^-53
+__host__ __device__ __forceinline__ double u64_to_unit_double(uint64_t x) {
+  return (double)(x >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// ---------------------------------------------------------------------------
+// PCG64 jump-ahead table: entry k holds (A_k, G_k) with
+//   state_k = A_k * state_0 + G_k * inc,  A_k = M^k,  G_k = sum_{j<k} M^j.
+// Entries 0..kJumpTable-1 are filled at library load.
+// ---------------------------------------------------------------------------
+constexpr int kJumpTable = 256;
+struct JumpEntry {
+  U128 a, g;
+};
+
+// ---------------------------------------------------------------------------
+// Job tables for the batched kernels.
+// ---------------------------------------------------------------------------
+constexpr int kMaxJobs = 48;
+
+struct QJob {
+  const void* x;          // segment input (element 0 of the segment)
+  uint8_t* codes[8];      // packed-code destinations (1..ndst copies, e.g. peers)
+  float* meta[8];         // per-bucket {shift, lo, hi} destinations
+  int64_t length;         // elements in the segment
+  int64_t global_start;   // key `start` of bucket 0 (sharded.py:243-248)
+  int64_t bucket_base;    // prefix: global bucket index of this job's bucket 0
+  SeedPrefix seed;        // root, step, layer, phase, worker already absorbed
+  int32_t ndst;
+  int32_t _pad;
+};
+
+struct QJobTable {
+  QJob jobs[kMaxJobs];
+  int32_t njobs;
+  int32_t bits;
+  int32_t bucket;
+  int32_t inner;
+  int64_t total_buckets;
+  unsigned long long* bad_index;  // atomicMin target: (job << 40) | element, or nullptr
+};
+
+struct DJob {
+  const uint8_t* codes[8];  // sources (1 for plain dequant; P for dequant-accumulate)
+  const float* meta[8];
+  void* out;
+  int64_t length;
+  int64_t bucket_base;
+  int32_t nsrc;
+  int32_t _pad;
+};
+
+struct DJobTable {
+  DJob jobs[kMaxJobs];
+  int32_t njobs;
+  int32_t bits;
+  int32_t bucket;
+  int32_t out_dtype;  // 0 f32, 1 f64, 2 bf16
+  int64_t total_buckets;
+  int32_t accumulate;  // 0: out = dequant(src0)  1: out = (0.0 + sum_p dequant(src_p)) / divisor
+  int32_t divisor;     // K4 divides the fp64 sum by this (the reference's `acc / P`)
+  int32_t codes_vec;   // 1: code groups may be read with aligned 2/4/8-byte loads
+  int32_t _pad2;
+};
+
+__host__ __device__ __forceinline__ int64_t payload_bytes(int64_t len, int bits) { return (len * bits + 7) / 8; }
+
+__device__ __forceinline__ int find_job_q(const QJobTable& t, int64_t b) {
+  int j = 0;
+  while (j + 1 < t.njobs && t.jobs[j + 1].bucket_base <= b) ++j;
+  return j;
+}
+__device__ __forceinline__ int find_job_d(const DJobTable& t, int64_t b) {
+  int j = 0;
+  while (j + 1 < t.njobs && t.jobs[j + 1].bucket_base <= b) ++j;
+  return j;
+}
+
+}  // namespace qsdp

@@ -1,0 +1,68 @@
+"""Multi-GPU check of QSDPComm (C1/C2 over NVLink peer memory); run with
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tests/dist_comm_check.py
+Every rank checks its all-gather output and its reduce-scatter shard bit-exactly
+against the oracle's single-process protocol (sharded.py:323-433)."""
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from oracle import oracle as O  # noqa: E402  (checker only)
+from paper_2302_02390_b200.comm import QSDPComm, plan_segments  # noqa: E402
+from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey  # noqa: E402
+
+
+def main():
+    dist.init_process_group("nccl")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    failures = 0
+    for size, bucket, wb, gb, pad in [(1 << 20, 1024, 8, 8, 1), (3 * 1024 * 1024 + 777, 1024, 8, 4, 1),
+                                      (1 << 22, 1024, 8, 8, 1024), (50000, 64, 6, 4, 1)]:
+        segs = plan_segments(size, world, pad)
+        maxseg = max(n for _, n in segs)
+        comm = QSDPComm(maxseg, QuantSpec(wb, bucket, "shift"), QuantSpec(gb, bucket, "uniform_stochastic"))
+        rng = np.random.default_rng(size)
+        full = (rng.standard_normal(size) * 0.02).astype(np.float32)
+        grads = [(np.random.default_rng(size + 1 + p).standard_normal(size) * 1e-3).astype(np.float32)
+                 for p in range(world)]
+        for step in range(3):
+            s, n = segs[rank]
+            shard = torch.from_numpy(full[s:s + n]).to(dev)
+            out = torch.empty(size, dtype=torch.float32, device=dev)
+            comm.all_gather(shard, segs, SegmentKey(0, step, 4, step % 2, 0), out)
+            exp = np.zeros(size)
+            for q, (sq, nq) in enumerate(segs):
+                if nq:
+                    c, m, _ = O.quantize_segment(full[sq:sq + nq], sq, bucket, wb, 0, (0, step, 4, step % 2, 0), 8)
+                    exp[sq:sq + nq] = O.dequantize_segment(c, m, nq, bucket, wb, 8)
+            ok_ag = np.array_equal(out.cpu().numpy(), exp.astype(np.float32))
+            g = torch.from_numpy(grads[rank]).to(dev)
+            sh = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+            comm.reduce_scatter(g, segs, SegmentKey(0, step, 4, 2, rank), sh)
+            acc = np.zeros(n)
+            for p in range(world):
+                if n:
+                    c, m, _ = O.quantize_segment(grads[p][s:s + n], s, bucket, gb, 1, (0, step, 4, 2, p), 8)
+                    acc = acc + O.dequantize_segment(c, m, n, bucket, gb, 8)
+            ok_rs = np.array_equal(sh[:n].cpu().numpy(), (acc / world).astype(np.float32))
+            if not (ok_ag and ok_rs):
+                failures += 1
+                print(f"rank {rank} size {size} step {step}: ag {ok_ag} rs {ok_rs}", flush=True)
+        comm.close()
+    t = torch.tensor([failures], device=dev)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(f"dist_comm_check world={world}: {'OK' if t.item() == 0 else 'FAILED'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if t.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+"""Generate golden vectors from the LIVE reference (run in the dev container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes tests/golden/golden.npz.  Every array is produced by the unmodified
+reference functions:
+
+* noise:    np.random.SeedSequence(key).generate_state(4, uint64) and the first
+            draws of bucket_rng(*key) (pkg/src/qsdp/sharded.py:235-240);
+* quant_*:  _segment_blocks(...) -> QuantizedBlock codes/scales/shift, encode()
+            wire bytes, dequantize() fp64 (quantize.py:209-286, wire.py:108-131,
+            sharded.py:243-248);
+* hook_*:   inputs/outputs of ShardedMLP._gather / ._reduce_scatter recorded
+            during a short ShardedMLP run (sharded.py:323-433), plus the run's
+            ledger bits and losses, and ReferenceMLP's final parameters.
+
+The fixtures travel to the GPU box (the reference does not); tests compare both
+the C oracle and the CUDA path against them.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+from qsdp.quantize import dequantize
+from qsdp.sharded import (
+    PHASE_GRAD,
+    QuantConfig,
+    ReferenceMLP,
+    ShardedMLP,
+    SimConfig,
+    _segment_blocks,
+    bucket_rng,
+)
+from qsdp.wire import _pack_codes, encode
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+
+
+def _cases():
+    """(bits, inner, bucket, n, start, key, dtype, distribution) quantizer cases."""
+    rng = np.random.default_rng(20230205)
+    cases = []
+    # The paper's configurations: w8 shift / g8, g4 stochastic, bucket 1024.
+    for bits, inner in [(8, "shift"), (8, "uniform_stochastic"), (4, "uniform_stochastic"),
+                        (4, "shift"), (6, "shift"), (5, "uniform_stochastic")]:
+        cases.append((bits, inner, 1024, 3000, 4096, (0, 3, 2, 0 if inner == "shift" else 2, 1),
+                      "f32", "normal"))
+    # bucket-size sweep 64..4096 (350M config), short last buckets, odd starts
+    for S in (64, 128, 256, 512, 2048, 4096):
+        cases.append((4, "uniform_stochastic", S, 5 * S + 17, 123457, (7, 1, 4, 2, 3), "f32", "normal"))
+        cases.append((8, "shift", S, 3 * S + 5, 999, (7, 1, 4, 1, 0), "f32", "normal"))
+    # every bit width 1..16, both modes, fp64 inputs (the reference's dtype)
+    for bits in range(1, 17):
+        for inner in ("shift", "uniform_stochastic"):
+            cases.append((bits, inner, 100, 333, int(rng.integers(0, 2**31)),
+                          (1, 2, 3, 0 if inner == "shift" else 2, 0), "f64", "normal"))
+    # stress: heavy tails, constant (degenerate) buckets, tiny ranges, large keys
+    cases.append((8, "shift", 1024, 4096, 0, (0, 0, 0, 0, 0), "f32", "student_t"))
+    cases.append((8, "uniform_stochastic", 1024, 4096, 0, (0, 0, 0, 2, 5), "f32", "constant_mix"))
+    cases.append((8, "shift", 1024, 2500, 2**33 + 5, (2**40 + 3, 2**35, 1, 0, 0), "f32", "tiny"))
+    cases.append((16, "uniform_stochastic", 1024, 2048, 77, (5, 9, 11, 2, 7), "f64", "normal"))
+    cases.append((8, "shift", 7, 50, 3, (1, 1, 1, 1, 0), "f64", "ties"))
+    return cases
+
+
+def _input(n, dtype, dist, rng):
+    if dist == "normal":
+        x = rng.standard_normal(n) * 0.02
+    elif dist == "student_t":
+        x = rng.standard_t(3, n) * 0.02
+    elif dist == "constant_mix":
+        x = rng.standard_normal(n) * 1e-3
+        x[1024:2048] = 0.25          # one fully degenerate bucket
+        x[3072:4096] = -0.0          # zeros
+    elif dist == "tiny":
+        x = (rng.standard_normal(n) * 1e-36)
+    elif dist == "ties":
+        x = np.tile(np.array([0.0, 0.5, 1.0, 1.5, 2.0, 2.5, 3.0]), n // 7 + 1)[:n]
+    else:
+        raise ValueError(dist)
+    if dtype == "f32":
+        x = x.astype(np.float32).astype(np.float64)
+    return x
+
+
+def main():
+    rng = np.random.default_rng(7)
+    out = {"numpy_version": np.array(np.__version__)}
+
+    # ---- noise -------------------------------------------------------------
+    keys = []
+    for k in range(64):
+        key = [int(v) for v in rng.integers(0, 2**31, 6)]
+        if k % 4 == 1:
+            key[5] = int(rng.integers(2**32, 2**40))     # start >= 2**32 (two words)
+        if k % 4 == 2:
+            key[0] = int(rng.integers(2**32, 2**62))     # large root seed
+        if k % 8 == 3:
+            key = [0, 0, 0, 0, 0, 0]
+        keys.append(key)
+    keys = np.array(keys, dtype=np.uint64)
+    states = np.stack([np.random.SeedSequence(tuple(int(v) for v in k)).generate_state(4, np.uint64)
+                       for k in keys])
+    draws = np.stack([bucket_rng(*[int(v) for v in k]).bit_generator.random_raw(8) for k in keys])
+    out.update(noise_keys=keys, noise_states=states, noise_draws=np.asarray(draws, dtype=np.uint64))
+
+    # ---- quantizer ---------------------------------------------------------
+    cases = _cases()
+    meta_rows = []
+    for i, (bits, inner, S, n, start, key, dtype, dist) in enumerate(cases):
+        x = _input(n, dtype, dist, rng)
+        blocks = _segment_blocks(x, start, S, bits, inner, lambda s: bucket_rng(*key, s))
+        codes = b"".join(_pack_codes(b.codes, bits) for b in blocks)
+        meta = np.array([[b.shift, b.scale_lo, b.scale_hi] for b in blocks], dtype=np.float32)
+        deq = np.concatenate([dequantize(b, inner) for b in blocks])
+        out[f"quant_{i}_x"] = x.astype(np.float32) if dtype == "f32" else x
+        out[f"quant_{i}_codes"] = np.frombuffer(codes, dtype=np.uint8)
+        out[f"quant_{i}_meta"] = meta
+        out[f"quant_{i}_deq"] = deq
+        out[f"quant_{i}_wire"] = np.frombuffer(encode(blocks), dtype=np.uint8)
+        meta_rows.append([bits, 0 if inner == "shift" else 1, S, n, start, *key])
+    out["quant_cases"] = np.array(meta_rows, dtype=np.int64)
+
+    # ---- protocol hooks: record a short ShardedMLP run ------------------------
+    hook_rows = []
+    hook_idx = 0
+    for P, quant in [(4, QuantConfig()), (2, QuantConfig(gradient_bits=4, bucket_size=64)),
+                     (3, QuantConfig(weight_bits=6, bucket_size=100))]:
+        cfg = SimConfig(widths=(64, 64, 10), P=P, batch=24, lr=0.05, quant=quant,
+                        root_seed=11, param_seed=11, data_seed=11)
+        sim = ShardedMLP(cfg)
+        rec = []
+        orig_g, orig_rs = sim._gather, sim._reduce_scatter
+
+        def g(step, layer_idx, phase, entry, _o=orig_g, _rec=rec, _sim=sim):
+            layer = _sim.layers[layer_idx]
+            shards = [s.copy() for s in _sim.model.shards[layer.name]]
+            res = _o(step, layer_idx, phase, entry)
+            _rec.append(("ag", step, layer_idx, phase, layer.kind, shards, res))
+            return res
+
+        def rs(step, layer_idx, grads, entry, _o=orig_rs, _rec=rec, _sim=sim):
+            layer = _sim.layers[layer_idx]
+            res = _o(step, layer_idx, grads, entry)
+            _rec.append(("rs", step, layer_idx, PHASE_GRAD, layer.kind,
+                         [np.asarray(gg).copy() for gg in grads], res))
+            return res
+
+        sim._gather, sim._reduce_scatter = g, rs
+        losses, bits_ag, bits_rs = [], [], []
+        for t in range(2):
+            loss, entry = sim.train_step(t)
+            losses.append(loss)
+            bits_ag.append(entry.allgather_bits)
+            bits_rs.append(entry.reducescatter_bits)
+        ref = ReferenceMLP(cfg)
+        ref_losses = ref.run(2)
+        assert ref_losses == losses
+        run_id = len(hook_rows)
+        for kind, step, li, phase, lkind, ins, res in rec:
+            if lkind != "dense":
+                continue   # exempt layers are raw copies; covered by host tests
+            out[f"hook_{hook_idx}_in"] = np.stack([np.asarray(v) for v in ins]) if kind == "rs" \
+                else np.concatenate(ins)
+            out[f"hook_{hook_idx}_out"] = np.concatenate(res) if kind == "rs" else res
+            out[f"hookmeta_{hook_idx}"] = np.array(
+                [run_id, 0 if kind == "ag" else 1, step, li, phase], dtype=np.int64)
+            hook_idx += 1
+        out[f"run_{run_id}_cfg"] = np.array(
+            [P, quant.weight_bits, quant.gradient_bits, quant.bucket_size, 11], dtype=np.int64)
+        out[f"run_{run_id}_losses"] = np.array(losses)
+        out[f"run_{run_id}_bits"] = np.array([bits_ag, bits_rs], dtype=np.int64)
+        for name, v in ref.params.items():
+            out[f"run_{run_id}_param_{name}"] = v
+        hook_rows.append(run_id)
+    out["n_hooks"] = np.array(hook_idx)
+    out["n_runs"] = np.array(len(hook_rows))
+    np.savez_compressed(OUT, **out)
+    print(f"wrote {OUT}: {os.path.getsize(OUT)/1e6:.2f} MB, {len(cases)} quant cases, "
+          f"{hook_idx} hook calls")
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,52 @@
+"""GPU: the C1/C2 communicator.  world=1 in-process; world>1 via torchrun when
+the box has several GPUs (tests/dist_comm_check.py)."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT
+from paper_2302_02390_b200.comm import QSDPComm, plan_segments
+from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey
+
+pytestmark = pytest.mark.gpu
+
+
+def test_single_rank_comm_vs_oracle(oracle):
+    dev = torch.device("cuda", 0)
+    size = 3 * 1024 * 100 + 11
+    comm = QSDPComm(size, QuantSpec(8, 1024, "shift"), QuantSpec(8, 1024, "uniform_stochastic"), device=dev)
+    x = (np.random.default_rng(1).standard_normal(size) * 0.02).astype(np.float32)
+    xt = torch.from_numpy(x).to(dev)
+    for step in range(3):
+        out = torch.empty(size, device=dev)
+        comm.all_gather(xt, [(0, size)], SegmentKey(0, step, 1, 0, 0), out)
+        c, m, _ = oracle.quantize_segment(x, 0, 1024, 8, 0, (0, step, 1, 0, 0), 8)
+        exp = oracle.dequantize_segment(c, m, size, 1024, 8, 8).astype(np.float32)
+        assert np.array_equal(out.cpu().numpy(), exp)
+        sh = torch.empty(size, device=dev)
+        comm.reduce_scatter(xt, [(0, size)], SegmentKey(0, step, 1, 2, 0), sh)
+        c, m, _ = oracle.quantize_segment(x, 0, 1024, 8, 1, (0, step, 1, 2, 0), 8)
+        exp = (np.zeros(size) + oracle.dequantize_segment(c, m, size, 1024, 8, 8)) / 1
+        assert np.array_equal(sh.cpu().numpy(), exp.astype(np.float32))
+    comm.close()
+
+
+def test_plan_segments():
+    assert plan_segments(10, 4) == [(0, 2), (2, 2), (4, 2), (6, 4)]
+    assert plan_segments(10, 4, pad_to=4) == [(0, 4), (4, 4), (8, 2), (10, 0)]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multi_gpu_comm():
+    n = min(4, torch.cuda.device_count())
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533",
+                        os.path.join(ROOT, "tests", "dist_comm_check.py")],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
