@@ -154,9 +154,8 @@ qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const q
       if (s.length <= 0) continue;
       QJob& J = tab.jobs[nj++];
       J.x = s.x;
-      J.codes[0] = s.codes;
-      J.meta[0] = s.meta;
-      J.ndst = 1;
+      J.codes = s.codes;
+      J.meta = s.meta;
       J.length = s.length;
       J.global_start = s.global_start;
       J.bucket_base = nb;

@@ -2,25 +2,34 @@
 #include "qsdp_kernels.cuh"
 
 namespace qsdp {
-template <int TL, int OUT, bool ACC>
+template <int BITS, int TL, int OUT, bool ACC>
 static cudaError_t launch_d_tl(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
   const int grid = grid_for(tab.total_buckets, 32 / TL, sms);
-  if (vec) dequant_kernel<TL, OUT, true, ACC><<<grid, 256, 0, s>>>(tab);
-  else dequant_kernel<TL, OUT, false, ACC><<<grid, 256, 0, s>>>(tab);
+  if (vec) dequant_kernel<BITS, TL, OUT, true, ACC><<<grid, 256, 0, s>>>(tab);
+  else dequant_kernel<BITS, TL, OUT, false, ACC><<<grid, 256, 0, s>>>(tab);
   return cudaGetLastError();
+}
+
+template <int BITS, int OUT, bool ACC>
+static cudaError_t launch_d_bits(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  int tl = team_lanes(tab.bucket);
+  if (ACC && tl < 8) tl = 8;  // per-source scale rows are filled by lanes 0..nsrc-1
+  switch (tl) {
+    case 1: return launch_d_tl<BITS, 1, OUT, ACC>(tab, vec, sms, s);
+    case 2: return launch_d_tl<BITS, 2, OUT, ACC>(tab, vec, sms, s);
+    case 4: return launch_d_tl<BITS, 4, OUT, ACC>(tab, vec, sms, s);
+    case 8: return launch_d_tl<BITS, 8, OUT, ACC>(tab, vec, sms, s);
+    case 16: return launch_d_tl<BITS, 16, OUT, ACC>(tab, vec, sms, s);
+    default: return launch_d_tl<BITS, 32, OUT, ACC>(tab, vec, sms, s);
+  }
 }
 
 template <int OUT, bool ACC>
 static cudaError_t launch_d_out(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
-  int tl = team_lanes(tab.bucket);
-  if (ACC && tl < 8) tl = 8;  // per-source scale rows are filled by lanes 0..nsrc-1
-  switch (tl) {
-    case 1: return launch_d_tl<1, OUT, ACC>(tab, vec, sms, s);
-    case 2: return launch_d_tl<2, OUT, ACC>(tab, vec, sms, s);
-    case 4: return launch_d_tl<4, OUT, ACC>(tab, vec, sms, s);
-    case 8: return launch_d_tl<8, OUT, ACC>(tab, vec, sms, s);
-    case 16: return launch_d_tl<16, OUT, ACC>(tab, vec, sms, s);
-    default: return launch_d_tl<32, OUT, ACC>(tab, vec, sms, s);
+  switch (tab.bits) {
+    case 8: return launch_d_bits<8, OUT, ACC>(tab, vec, sms, s);
+    case 4: return launch_d_bits<4, OUT, ACC>(tab, vec, sms, s);
+    default: return launch_d_bits<0, OUT, ACC>(tab, vec, sms, s);
   }
 }
 

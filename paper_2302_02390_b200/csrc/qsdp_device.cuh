@@ -152,18 +152,16 @@ struct JumpEntry {
 // ---------------------------------------------------------------------------
 // Job tables for the batched kernels.
 // ---------------------------------------------------------------------------
-constexpr int kMaxJobs = 48;
+constexpr int kMaxJobs = 64;
 
 struct QJob {
   const void* x;          // segment input (element 0 of the segment)
-  uint8_t* codes[8];      // packed-code destinations (1..ndst copies, e.g. peers)
-  float* meta[8];         // per-bucket {shift, lo, hi} destinations
+  uint8_t* codes;         // packed-code output
+  float* meta;            // per-bucket {shift, lo, hi}
   int64_t length;         // elements in the segment
   int64_t global_start;   // key `start` of bucket 0 (sharded.py:243-248)
   int64_t bucket_base;    // prefix: global bucket index of this job's bucket 0
   SeedPrefix seed;        // root, step, layer, phase, worker already absorbed
-  int32_t ndst;
-  int32_t _pad;
 };
 
 struct QJobTable {

@@ -13,8 +13,13 @@
 //
 // Thread mapping: one "team" of TL lanes (TL = min(32, pow2ceil(S/4))) owns a
 // bucket; lane t of the team owns element groups g*TL + t of 4 consecutive
-// elements, so every warp-wide load is one fully coalesced 128-bit access per
-// lane.  Min/max are team-reduced with xor shuffles; no shared memory.
+// elements, so every warp-wide access is fully coalesced.  Min/max are
+// team-reduced with xor shuffles on order-preserving integer keys.
+//
+// Fast quantizer (quantize_tma_kernel, widths 2/4/8/16): every warp runs its
+// own NST-stage pipeline -- one elected lane streams whole buckets into a
+// shared-memory ring with cp.async.bulk (TMA bulk copies completing on an
+// mbarrier) NST buckets ahead, so HBM reads overlap the code computation.
 //
 // Exactness: the reference computes in IEEE binary64 (u = (v-lo)/(hi-lo),
 // (u-r)/pitch, round-half-even; u*top, floor, d < frac).  Each element is first
@@ -40,41 +45,48 @@ static __device__ JumpEntry g_jump[kJumpTable];
 // 1.5 * 2^20: adding it rounds to multiples of 2^-32, so the low mantissa bits
 // hold round(w * 2^32) for |w| < 2^19 (32.32 fixed point, no F2I needed).
 constexpr double kMagic32 = 1572864.0;
-constexpr uint64_t kMantMask = (1ull << 52) - 1;
-constexpr int64_t kMantBias = 1ll << 51;
 
-__device__ __forceinline__ int64_t fixed32(double w) {
+struct Fixed32 {
+  uint32_t frac;  // low 32 bits of round(w * 2^32)
+  int32_t ip;     // floor of the rounded value (integer part), |ip| < 2^19
+};
+__device__ __forceinline__ Fixed32 fixed32(double w) {
   const double y = __dadd_rn(w, kMagic32);
-  return (int64_t)(__double_as_longlong(y) & kMantMask) - kMantBias;
-}
-
-__device__ __forceinline__ bool finite_f(float v) { return (__float_as_uint(v) & 0x7f800000u) != 0x7f800000u; }
-__device__ __forceinline__ bool finite_d(double v) {
-  return ((unsigned long long)__double_as_longlong(v) & 0x7ff0000000000000ull) != 0x7ff0000000000000ull;
+  const uint32_t lo = (uint32_t)__double2loint(y);
+  const uint32_t hi = (uint32_t)__double2hiint(y);
+  // mantissa = 2^51 + round(w*2^32): integer part sits in hi bits [0, 20) offset by 2^19
+  return Fixed32{lo, (int32_t)(hi & 0xFFFFFu) - (1 << 19)};
 }
 
 // Min/max run on order-preserving integer keys of the IEEE bits (total order,
 // -0.0 < +0.0): integer IMNMX instead of float compares, and a zero extremum
 // keeps numpy's sign when the bucket's zero extremum has a single sign.
+// Non-finite values map outside [key(-inf), key(+inf)] exclusive bounds, so a
+// bucket is finite iff key(-inf) < min_key and max_key < key(+inf).
 template <typename T>
 struct InTraits;
 template <>
 struct InTraits<float> {
   using Key = int32_t;
-  __device__ static __forceinline__ bool finite(float v) { return finite_f(v); }
   __device__ static __forceinline__ double to_d(float v) { return (double)v; }
+  __device__ static __forceinline__ bool finite(float v) {
+    return (__float_as_uint(v) & 0x7f800000u) != 0x7f800000u;
+  }
   __device__ static __forceinline__ Key key(float v) {
     const int32_t b = __float_as_int(v);
     return b ^ ((b >> 31) & 0x7fffffff);
   }
   __device__ static __forceinline__ float from_key(Key k) { return __int_as_float(k ^ ((k >> 31) & 0x7fffffff)); }
   static constexpr Key kMax = 0x7fffffff, kMin = (int32_t)0x80000000;
+  static constexpr Key kPosInf = 0x7f800000, kNegInf = (int32_t)0x807fffff;
 };
 template <>
 struct InTraits<double> {
   using Key = long long;
-  __device__ static __forceinline__ bool finite(double v) { return finite_d(v); }
   __device__ static __forceinline__ double to_d(double v) { return v; }
+  __device__ static __forceinline__ bool finite(double v) {
+    return ((unsigned long long)__double_as_longlong(v) & 0x7ff0000000000000ull) != 0x7ff0000000000000ull;
+  }
   __device__ static __forceinline__ Key key(double v) {
     const long long b = __double_as_longlong(v);
     return b ^ ((b >> 63) & 0x7fffffffffffffffll);
@@ -83,9 +95,10 @@ struct InTraits<double> {
     return __longlong_as_double(k ^ ((k >> 63) & 0x7fffffffffffffffll));
   }
   static constexpr Key kMax = 0x7fffffffffffffffll, kMin = (long long)0x8000000000000000ull;
+  static constexpr Key kPosInf = 0x7ff0000000000000ll, kNegInf = (long long)0x800fffffffffffffull;
 };
 
-// Streaming 128-bit loads (no L1 allocation) when the bucket stays in registers;
+// Streaming 128-bit loads (no L1 allocation) when a value is read once;
 // cached loads when the bucket is re-read in a second pass.
 template <bool STREAM>
 __device__ __forceinline__ float4 ld4(const float* p) {
@@ -123,6 +136,19 @@ __device__ __forceinline__ void load_group(const T* x, int e, int n, T v[4]) {
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i) v[i] = (e + i < n) ? x[e + i] : T(0);
+  }
+}
+
+// 4 consecutive elements from shared memory (16-byte aligned group).
+template <typename T>
+__device__ __forceinline__ void lds_group(const T* s, int e, T v[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 f = *reinterpret_cast<const float4*>(s + e);
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  } else {
+    const double2 a = *reinterpret_cast<const double2*>(s + e);
+    const double2 b = *reinterpret_cast<const double2*>(s + e + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
   }
 }
 
@@ -174,89 +200,340 @@ __host__ __device__ __forceinline__ bool direct_width(int bits) {
   return bits == 8 || bits == 4 || bits == 16 || bits == 2;
 }
 
-// Store the packed bits of element group gi (4 codes, LSB-first) of a bucket.
-// `w` holds this lane's 4*bits bits; `other` the partner lane's (gi^1), used
-// when a group of 4 codes does not fill whole bytes (8 codes = `bits` bytes).
-// `pbytes` bounds the writes for the bucket's final partial group.
-__device__ __forceinline__ void store_group(uint8_t* const* dst, int ndst, int64_t boff, int gi, uint64_t w,
-                                            uint64_t other, int bits, int64_t pbytes, bool full) {
-  if (direct_width(bits)) {
-    const int nb = bits / 2;  // bytes per group of 4 codes
-    const int64_t o = boff + (int64_t)gi * nb;
-    if (full) {
-      for (int d = 0; d < ndst; ++d) {
-        uint8_t* p = dst[d] + o;
-        if (bits == 8) *reinterpret_cast<uint32_t*>(p) = (uint32_t)w;
-        else if (bits == 4) *reinterpret_cast<uint16_t*>(p) = (uint16_t)w;
-        else if (bits == 16) *reinterpret_cast<unsigned long long*>(p) = w;
-        else *p = (uint8_t)w;
+// ---------------------------------------------------------------------------
+// Per-bucket quantization context and the per-element certified fast path.
+// ---------------------------------------------------------------------------
+template <typename T, int INNER>
+struct Coder {
+  double lo, span, inv, pitch, top, r;
+  U128 st, inc, jmp_a, jmp_c;
+
+  // Bucket setup: scales, noise.  `lt` = lane in team, TL = team lanes.
+  __device__ __forceinline__ void setup(float lof, float hif, int bits, const SeedPrefix& seed, uint64_t start,
+                                        int lt, int TL, float& shift_f) {
+    top = (double)((1u << bits) - 1u);
+    lo = (double)lof;
+    span = __dsub_rn((double)hif, lo);
+    inv = __drcp_rn(span);
+    pitch = __ddiv_rn(1.0, top);
+    r = 0.0;
+    seed_bucket(seed, start, st, inc);
+    if (INNER == 0) {
+      // sample_shift(pitch): uniform(-p/2, p/2) = -p/2 + p*d, unfused (quantize.py:130-132)
+      const U128 s1 = mad128(st, pcg_mult(), inc);
+      const double d = u64_to_unit_double(pcg_output(s1));
+      r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));
+      shift_f = __double2float_rn(__dmul_rn(r, span));  // _f32(r*(hi-lo))
+    } else {
+      // element e consumes draw e = out(state_{e+1}); lane starts at 4*lt, jumps 4*TL-3 per group
+      const JumpEntry e0 = g_jump[4 * lt + 1];
+      st = add128(mul128(e0.a, st), mul128(e0.g, inc));
+      const JumpEntry ej = g_jump[4 * TL - 3];
+      jmp_a = ej.a;
+      jmp_c = mul128(ej.g, inc);
+      shift_f = 0.0f;
+    }
+  }
+
+  // Code of one element; for INNER 1 uses the current state (caller steps it).
+  __device__ __forceinline__ uint32_t code(T t) {
+    const double a = __dsub_rn(InTraits<T>::to_d(t), lo);
+    if (INNER == 0) {
+      double u = __dmul_rn(a, inv);
+      if constexpr (sizeof(T) == 8) u = fmin(fmax(u, 0.0), 1.0);
+      const Fixed32 q = fixed32(__dmul_rn(__dsub_rn(u, r), top));
+      // |w - w_fast| * 2^32 + rounding < 2: decided unless frac within 2 of 1/2
+      if (q.frac - 0x7ffffffeu <= 3u) return exact_shift_code(a, span, r, pitch, top);
+      const int k = q.ip + (q.frac > 0x80000000u ? 1 : 0);
+      return (uint32_t)min(max(k, 0), (int)top);
+    } else {
+      const bool at_hi = a >= span;
+      const bool at_lo = a <= 0.0;
+      const double u = at_hi ? 1.0 : (at_lo ? 0.0 : __dmul_rn(a, inv));
+      const Fixed32 q = fixed32(__dmul_rn(u, top));
+      const uint32_t dh = pcg_output_hi32(st);
+      if (at_hi || at_lo) return (uint32_t)q.ip;  // s exact integer, frac 0: d < 0 is false
+      // uncertain iff fq in {dh, dh+1} or the floor itself is uncertain (fq == 0)
+      if (q.frac == 0u || q.frac - dh <= 1u) return exact_stoch_code(a, span, top, st);
+      const int c = q.ip + (q.frac > dh ? 1 : 0);
+      return (uint32_t)min(c, (int)top);
+    }
+  }
+
+  __device__ __forceinline__ void step() { st = mad128(st, pcg_mult(), inc); }
+  __device__ __forceinline__ void jump() { st = add128(mul128(jmp_a, st), jmp_c); }
+
+  // 4 codes of group starting at element e (elements >= n coded 0), packed LSB-first.
+  __device__ __forceinline__ uint64_t group(const T v[4], int e, int n, int bits) {
+    uint64_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t c = code(v[i]);
+      if (INNER == 1 && i < 3) step();
+      c = (e + i < n) ? c : 0u;
+      w |= (uint64_t)c << (i * bits);
+    }
+    if (INNER == 1) jump();
+    return w;
+  }
+};
+
+// Store the packed bits (b/2 bytes) of group gi for the direct widths.
+template <int BITS>
+__device__ __forceinline__ void store_direct(uint8_t* base, int gi, uint64_t w, int64_t pbytes, bool full) {
+  constexpr int NB = BITS / 2;
+  uint8_t* p = base + (int64_t)gi * NB;
+  if (full) {
+    if (BITS == 8) *reinterpret_cast<uint32_t*>(p) = (uint32_t)w;
+    else if (BITS == 4) *reinterpret_cast<uint16_t*>(p) = (uint16_t)w;
+    else if (BITS == 16) *reinterpret_cast<unsigned long long*>(p) = w;
+    else *p = (uint8_t)w;
+  } else {
+    const int64_t o = (int64_t)gi * NB;
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      if (o + k < pbytes) p[k] = (uint8_t)(w >> (8 * k));
+  }
+}
+
+// First non-finite element of a bucket (rare path): team-serial scan.
+template <typename T>
+__device__ __noinline__ int first_nonfinite(const T* x, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!InTraits<T>::finite(x[i])) return i;
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier / TMA bulk-copy primitives (sm_90+ PTX, native on sm_100a).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Resolve global bucket b of a job table.
+struct BucketRef {
+  int j;
+  int n;
+  int64_t lb, off;
+};
+__device__ __forceinline__ BucketRef resolve_q(const QJobTable& tab, int64_t b, int S) {
+  BucketRef r;
+  r.j = find_job_q(tab, b);
+  const QJob& J = tab.jobs[r.j];
+  r.lb = b - J.bucket_base;
+  r.off = r.lb * S;
+  r.n = (int)min((int64_t)S, J.length - r.off);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// K1/K2 fast path: TMA-pipelined quantizer for the direct widths.
+// Requirements (host-checked): BITS in {2,4,8,16}, S % 8 == 0, S*sizeof(T) <= 8 KB.
+// Dynamic smem: [warps][NST] stages of TEAMS*S elements, then [warps][NST] mbarriers.
+// ---------------------------------------------------------------------------
+template <typename T, int INNER, int BITS, int TL, int NST>
+__global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant__ QJobTable tab, int vec) {
+  constexpr int TEAMS = 32 / TL;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int S = tab.bucket;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int wpc = blockDim.x >> 5;
+  const int lt = lane % TL;
+  const int team = lane / TL;
+  const int64_t stage_elems = (int64_t)TEAMS * S;
+  T* wbuf = reinterpret_cast<T*>(smem) + (int64_t)wib * NST * stage_elems;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)wpc * NST * stage_elems * sizeof(T)) + wib * NST;
+  const int64_t gw = (int64_t)blockIdx.x * wpc + wib;
+  const int64_t nw = (int64_t)gridDim.x * wpc;
+  const int64_t total = tab.total_buckets;
+  const int64_t pbs = payload_bytes(S, BITS);
+  const int gl = (S / 4 + TL - 1) / TL;
+  using Tr = InTraits<T>;
+  using K = typename Tr::Key;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], TEAMS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  // Issue the bulk copy of iteration k into stage k % NST (team leaders).
+  auto issue = [&](int64_t k) {
+    const int64_t b = (gw + k * nw) * TEAMS + team;
+    if (lt == 0) {
+      uint64_t* bar = &bars[k % NST];
+      uint32_t bytes = 0;
+      const void* src = nullptr;
+      if (b < total) {
+        const BucketRef br = resolve_q(tab, b, S);
+        if (vec && br.n == S) {
+          bytes = (uint32_t)(S * sizeof(T));
+          src = reinterpret_cast<const T*>(tab.jobs[br.j].x) + br.off;
+        }
+      }
+      mbar_arrive_tx(bar, bytes);
+      if (bytes) tma_load_1d(wbuf + (k % NST) * stage_elems + (int64_t)team * S, src, bytes, bar);
+    }
+  };
+
+  for (int64_t k = 0; k < NST; ++k)
+    if ((gw + k * nw) * TEAMS < total) issue(k);
+
+  for (int64_t k = 0; (gw + k * nw) * TEAMS < total; ++k) {
+    const int stage = (int)(k % NST);
+    mbar_wait(&bars[stage], (uint32_t)((k / NST) & 1));
+    const T* sb = wbuf + stage * stage_elems + (int64_t)team * S;
+    const int64_t b = (gw + k * nw) * TEAMS + team;
+    const bool active = b < total;
+    BucketRef br{0, 0, 0, 0};
+    if (active) br = resolve_q(tab, b, S);
+    const QJob& J = tab.jobs[br.j];
+    const int n = br.n;
+    const bool in_smem = vec && n == S;
+    const T* gx = reinterpret_cast<const T*>(J.x) + br.off;
+
+    // ---- pass 1: min/max keys ------------------------------------------------
+    K mnk = Tr::kMax, mxk = Tr::kMin;
+    if (in_smem) {
+      for (int g = 0; g < gl; ++g) {
+        const int e = 4 * (g * TL + lt);
+        if (e < n) {
+          T v[4];
+          lds_group(sb, e, v);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const K kk = Tr::key(v[i]);
+            mnk = min(mnk, kk);
+            mxk = max(mxk, kk);
+          }
+        }
       }
     } else {
-      const int64_t lim = boff + pbytes;
-      for (int d = 0; d < ndst; ++d)
-        for (int k = 0; k < nb; ++k)
-          if (o + k < lim) dst[d][o + k] = (uint8_t)(w >> (8 * k));
+      for (int g = 0; g < gl; ++g) {
+        const int e = 4 * (g * TL + lt);
+        if (e < n) {
+          T v[4];
+          load_group<T, false, false>(gx, e, n, v);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (e + i < n) {
+              const K kk = Tr::key(v[i]);
+              mnk = min(mnk, kk);
+              mxk = max(mxk, kk);
+            }
+          }
+        }
+      }
     }
+    mnk = team_min_k<TL>(mnk);
+    mxk = team_max_k<TL>(mxk);
+    const bool nonfinite = active && n > 0 && !(Tr::kNegInf < mnk && mxk < Tr::kPosInf);
+    const float lof = nonfinite ? 0.0f : (float)Tr::to_d(Tr::from_key(mnk));  // _f32(min)
+    const float hif = nonfinite ? 0.0f : (float)Tr::to_d(Tr::from_key(mxk));  // _f32(max)
+    const bool degenerate = nonfinite || !(lof < hif);                        // quantize.py:254-264
+    if (nonfinite && lt == 0 && tab.bad_index != nullptr) {
+      const int i = first_nonfinite<T>(in_smem ? sb : gx, n);
+      atomicMin(tab.bad_index, ((unsigned long long)br.j << 40) | (unsigned long long)(br.off + i));
+    }
+
+    // ---- pass 2: codes ----------------------------------------------------------
+    Coder<T, INNER> cd;
+    float shift_f = 0.0f;
+    if (active && !degenerate) cd.setup(lof, hif, BITS, J.seed, (uint64_t)(J.global_start + br.off), lt, TL, shift_f);
+    uint8_t* cbase = J.codes + br.lb * pbs;
+    const int64_t pb = payload_bytes(n, BITS);
+    if (active && !degenerate && in_smem) {
+      for (int g = 0; g < gl; ++g) {
+        const int gi = g * TL + lt;
+        const int e = 4 * gi;
+        if (e < n) {
+          T v[4];
+          lds_group(sb, e, v);
+          store_direct<BITS>(cbase, gi, cd.group(v, e, n, BITS), pb, true);
+        }
+      }
+    } else if (active) {
+      for (int g = 0; g < gl; ++g) {
+        const int gi = g * TL + lt;
+        const int e = 4 * gi;
+        if (e < n) {
+          uint64_t w = 0;
+          if (!degenerate) {
+            T v[4];
+            load_group<T, false, false>(gx, e, n, v);
+            w = cd.group(v, e, n, BITS);
+          }
+          store_direct<BITS>(cbase, gi, w, pb, e + 4 <= n);
+        }
+      }
+    }
+    if (active && lt == 0) {
+      float* m = J.meta + 3 * br.lb;
+      m[0] = degenerate ? 0.0f : shift_f;
+      m[1] = lof;
+      m[2] = hif;
+    }
+    // release the stage to the async proxy, then refill it NST iterations ahead
+    __syncwarp();
+    fence_proxy_async();
+    if ((gw + (k + NST) * nw) * TEAMS < total) issue(k + NST);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1/K2 for any width 1..16 (odd widths merge lane pairs into whole bytes),
+// S % 8 == 0.  Registers hold up to G groups per lane (HOLD) or the bucket is
+// re-read (second pass through L1/L2).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void store_pair(uint8_t* cbase, int gi, uint64_t w, uint64_t other, int bits,
+                                           int64_t pbytes) {
+  if (direct_width(bits)) {
+    const int nb = bits / 2;
+    const int64_t o = (int64_t)gi * nb;
+    for (int k = 0; k < nb; ++k)
+      if (o + k < pbytes) cbase[o + k] = (uint8_t)(w >> (8 * k));
     return;
   }
   if ((gi & 1) == 0) {
     const int sh = 4 * bits;  // < 64 for the widths routed here
     const uint64_t lo = w | (other << sh);
     const uint64_t hi = other >> (64 - sh);
-    const int64_t o = boff + (int64_t)(gi >> 1) * bits;
-    const int64_t lim = boff + pbytes;
-    for (int d = 0; d < ndst; ++d)
-      for (int k = 0; k < bits; ++k) {
-        if (o + k >= lim) break;
-        const uint64_t word = k < 8 ? lo : hi;
-        dst[d][o + k] = (uint8_t)(word >> (8 * (k & 7)));
-      }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K1/K2: batched bucket quantizer.
-// INNER 0 = shift (weights), 1 = uniform_stochastic/flip (gradients).
-// G = element groups per lane kept in registers (HOLD) or re-read (!HOLD).
-// ---------------------------------------------------------------------------
-// Per-element code: certified division-free fast path, exact fallback.
-template <typename T, int INNER>
-struct Coder {
-  double lo, span, inv, pitch, top, r;
-  U128 st, inc;
-
-  __device__ __forceinline__ uint32_t code(T t) {
-    const double a = __dsub_rn(InTraits<T>::to_d(t), lo);
-    if (INNER == 0) {
-      double u = __dmul_rn(a, inv);
-      if constexpr (sizeof(T) == 8) u = fmin(fmax(u, 0.0), 1.0);
-      const double wv = __dmul_rn(__dsub_rn(u, r), top);
-      const int64_t q = fixed32(wv);
-      const uint32_t fr = (uint32_t)q;
-      if (fr - 0x7ffffffeu <= 3u) return exact_shift_code(a, span, r, pitch, top);  // |fr-2^31|<=2
-      const int64_t k = (q >> 32) + (fr > 0x80000000u ? 1 : 0);
-      return (uint32_t)(k < 0 ? 0 : (k > (int64_t)top ? (int64_t)top : k));
-    } else {
-      const bool at_hi = a >= span;
-      const bool at_lo = a <= 0.0;
-      const double u = at_hi ? 1.0 : (at_lo ? 0.0 : __dmul_rn(a, inv));
-      const int64_t q = fixed32(__dmul_rn(u, top));
-      const uint32_t fq = (uint32_t)q;
-      const int64_t nfl = q >> 32;
-      const uint32_t dh = pcg_output_hi32(st);
-      uint32_t c;
-      if (at_hi || at_lo) {
-        c = (uint32_t)nfl;  // s is an exact integer, frac 0: d < 0 is false
-      } else if (fq == 0u || fq - dh <= 1u) {
-        c = exact_stoch_code(a, span, top, st);  // fq in {dh, dh+1} or floor uncertain
-      } else {
-        const int64_t cc = nfl + (fq > dh ? 1 : 0);
-        c = (uint32_t)(cc > (int64_t)top ? (int64_t)top : cc);
-      }
-      return c;
+    const int64_t o = (int64_t)(gi >> 1) * bits;
+    for (int k = 0; k < bits; ++k) {
+      if (o + k >= pbytes) break;
+      const uint64_t word = k < 8 ? lo : hi;
+      cbase[o + k] = (uint8_t)(word >> (8 * (k & 7)));
     }
   }
-};
+}
 
 template <typename T, int INNER, int TL, int G, bool HOLD, bool VEC>
 __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ QJobTable tab) {
@@ -269,39 +546,31 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
   const int S = tab.bucket;
   const int bits = tab.bits;
   const bool pair = !direct_width(bits);
-  const double top = (double)((1u << bits) - 1u);
   const int64_t pbs = payload_bytes(S, bits);
   const int groups = (S + 3) / 4;
-  const int gl = (groups + TL - 1) / TL;  // groups per lane (<= G when HOLD)
+  const int gl = (groups + TL - 1) / TL;
+  using Tr = InTraits<T>;
+  using K = typename Tr::Key;
 
   for (int64_t b0 = warp * TEAMS; b0 < tab.total_buckets; b0 += nwarps * TEAMS) {
     const int64_t b = b0 + team;
     const bool active = b < tab.total_buckets;
-    const int j = active ? find_job_q(tab, b) : 0;
-    const QJob& J = tab.jobs[j];
-    const int64_t lb = active ? b - J.bucket_base : 0;
-    const int64_t off = lb * S;
-    const int n = active ? (int)min((int64_t)S, J.length - off) : 0;
-    const T* x = reinterpret_cast<const T*>(J.x) + off;
+    BucketRef br{0, 0, 0, 0};
+    if (active) br = resolve_q(tab, b, S);
+    const QJob& J = tab.jobs[br.j];
+    const int n = br.n;
+    const T* x = reinterpret_cast<const T*>(J.x) + br.off;
 
-    // ---- pass 1: load, finiteness, min/max (quantize.py:41-44, 251-252) ----
-    using K = typename InTraits<T>::Key;
     T v[HOLD ? G : 1][4];
-    K mnk = InTraits<T>::kMax, mxk = InTraits<T>::kMin;
-    int bad = 0x7fffffff;
+    K mnk = Tr::kMax, mxk = Tr::kMin;
     auto scan = [&](const T t[4], int e) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 4; ++i)
         if (e + i < n) {
-          if (InTraits<T>::finite(t[i])) {
-            const K kk = InTraits<T>::key(t[i]);
-            mnk = min(mnk, kk);
-            mxk = max(mxk, kk);
-          } else {
-            bad = min(bad, e + i);
-          }
+          const K kk = Tr::key(t[i]);
+          mnk = min(mnk, kk);
+          mxk = max(mxk, kk);
         }
-      }
     };
     if constexpr (HOLD) {
 #pragma unroll
@@ -324,62 +593,38 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
     }
     mnk = team_min_k<TL>(mnk);
     mxk = team_max_k<TL>(mxk);
-    bad = team_min_i<TL>(bad);
-
-    // lo/hi = _f32(min/max)  (quantize.py:251-252)
-    const float lof = (float)InTraits<T>::to_d(InTraits<T>::from_key(mnk));
-    const float hif = (float)InTraits<T>::to_d(InTraits<T>::from_key(mxk));
-    const bool nonfinite = bad != 0x7fffffff;
-    const bool degenerate = nonfinite || !(lof < hif);  // quantize.py:254-264
-    if (active && nonfinite && lt == 0 && tab.bad_index != nullptr)
-      atomicMin(tab.bad_index, ((unsigned long long)j << 40) | (unsigned long long)(off + bad));
-
-    Coder<T, INNER> cd;
-    cd.lo = (double)lof;
-    cd.span = __dsub_rn((double)hif, cd.lo);
-    cd.inv = __drcp_rn(cd.span);
-    cd.top = top;
-    cd.pitch = __ddiv_rn(1.0, top);
-    cd.r = 0.0;
-    cd.st = U128{0, 0};
-    cd.inc = U128{0, 0};
-    U128 jmp_a{0, 0}, jmp_c{0, 0};
-    float shift_f = 0.0f;
-    if (active && !degenerate) {
-      seed_bucket(J.seed, (uint64_t)(J.global_start + off), cd.st, cd.inc);
-      if (INNER == 0) {
-        // sample_shift(pitch): uniform(-p/2, p/2) = -p/2 + p*d, unfused (quantize.py:130-132)
-        const U128 s1 = mad128(cd.st, pcg_mult(), cd.inc);
-        const double d = u64_to_unit_double(pcg_output(s1));
-        cd.r = __dadd_rn(__dmul_rn(cd.pitch, -0.5), __dmul_rn(cd.pitch, d));
-        shift_f = __double2float_rn(__dmul_rn(cd.r, cd.span));  // _f32(r*(hi-lo))
-      } else {
-        // element e consumes draw e = out(state_{e+1}); lane starts at 4*lt, jumps 4*TL-3
-        const JumpEntry e0 = g_jump[4 * lt + 1];
-        cd.st = add128(mul128(e0.a, cd.st), mul128(e0.g, cd.inc));
-        const JumpEntry ej = g_jump[4 * TL - 3];
-        jmp_a = ej.a;
-        jmp_c = mul128(ej.g, cd.inc);
-      }
+    const bool nonfinite = active && n > 0 && !(Tr::kNegInf < mnk && mxk < Tr::kPosInf);
+    const float lof = nonfinite ? 0.0f : (float)Tr::to_d(Tr::from_key(mnk));
+    const float hif = nonfinite ? 0.0f : (float)Tr::to_d(Tr::from_key(mxk));
+    const bool degenerate = nonfinite || !(lof < hif);
+    if (nonfinite && lt == 0 && tab.bad_index != nullptr) {
+      const int i = first_nonfinite<T>(x, n);
+      atomicMin(tab.bad_index, ((unsigned long long)br.j << 40) | (unsigned long long)(br.off + i));
     }
 
-    // ---- pass 2: codes + LSB-first packing --------------------------------
+    Coder<T, INNER> cd;
+    float shift_f = 0.0f;
+    if (active && !degenerate) cd.setup(lof, hif, bits, J.seed, (uint64_t)(J.global_start + br.off), lt, TL, shift_f);
+    uint8_t* cbase = J.codes + br.lb * pbs;
+    const int64_t pb = payload_bytes(n, bits);
     auto emit = [&](const T t[4], int g) {
       const int gi = g * TL + lt;
       const int e = 4 * gi;
       uint64_t w = 0;
-      if (!degenerate && e < n) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t c = cd.code(t[i]);
-          if (INNER == 1 && i < 3) cd.st = mad128(cd.st, pcg_mult(), cd.inc);
-          if (e + i >= n) c = 0;
-          w |= (uint64_t)c << (i * bits);
-        }
-        if (INNER == 1) cd.st = add128(mul128(jmp_a, cd.st), jmp_c);
-      }
+      if (!degenerate && e < n) w = cd.group(t, e, n, bits);
       const uint64_t other = pair ? __shfl_xor_sync(0xffffffffu, w, 1) : 0ull;
-      if (active && e < n) store_group(J.codes, J.ndst, lb * pbs, gi, w, other, bits, payload_bytes(n, bits), e + 4 <= n);
+      if (active && e < n) {
+        if (!pair && e + 4 <= n) {
+          const int nb = bits / 2;
+          uint8_t* p = cbase + (int64_t)gi * nb;
+          if (bits == 8) *reinterpret_cast<uint32_t*>(p) = (uint32_t)w;
+          else if (bits == 4) *reinterpret_cast<uint16_t*>(p) = (uint16_t)w;
+          else if (bits == 16) *reinterpret_cast<unsigned long long*>(p) = w;
+          else *p = (uint8_t)w;
+        } else {
+          store_pair(cbase, gi, w, other, bits, pb);
+        }
+      }
     };
     if constexpr (HOLD) {
 #pragma unroll
@@ -394,14 +639,10 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
       }
     }
     if (active && lt == 0) {
-      const float sh = degenerate ? 0.0f : shift_f;
-      const float l = nonfinite ? 0.0f : lof, h = nonfinite ? 0.0f : hif;
-      for (int d = 0; d < J.ndst; ++d) {
-        float* m = J.meta[d] + 3 * lb;
-        m[0] = sh;
-        m[1] = l;
-        m[2] = h;
-      }
+      float* m = J.meta + 3 * br.lb;
+      m[0] = degenerate ? 0.0f : shift_f;
+      m[1] = lof;
+      m[2] = hif;
     }
   }
 }
@@ -417,33 +658,33 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
   const int S = tab.bucket, bits = tab.bits;
   const double top = (double)((1u << bits) - 1u);
   const int64_t pbs = payload_bytes(S, bits);
+  using Tr = InTraits<T>;
+  using K = typename Tr::Key;
   for (int64_t b = tid; b < tab.total_buckets; b += nth) {
-    const int j = find_job_q(tab, b);
-    const QJob& J = tab.jobs[j];
-    const int64_t lb = b - J.bucket_base, off = lb * S;
-    const int n = (int)min((int64_t)S, J.length - off);
-    const T* x = reinterpret_cast<const T*>(J.x) + off;
-    using K = typename InTraits<T>::Key;
-    K mnk = InTraits<T>::kMax, mxk = InTraits<T>::kMin;
+    const BucketRef br = resolve_q(tab, b, S);
+    const QJob& J = tab.jobs[br.j];
+    const int n = br.n;
+    const T* x = reinterpret_cast<const T*>(J.x) + br.off;
+    K mnk = Tr::kMax, mxk = Tr::kMin;
     int bad = -1;
     for (int i = 0; i < n; ++i) {
       const T t = x[i];
-      if (!InTraits<T>::finite(t)) { bad = i; break; }
-      mnk = min(mnk, InTraits<T>::key(t));
-      mxk = max(mxk, InTraits<T>::key(t));
+      if (!Tr::finite(t)) { bad = i; break; }
+      mnk = min(mnk, Tr::key(t));
+      mxk = max(mxk, Tr::key(t));
     }
-    const float lof = (float)InTraits<T>::to_d(InTraits<T>::from_key(mnk));
-    const float hif = (float)InTraits<T>::to_d(InTraits<T>::from_key(mxk));
-    const double lo = lof, hi = hif;
-    const bool degenerate = bad >= 0 || !(lo < hi);
+    const float lof = bad >= 0 ? 0.0f : (float)Tr::to_d(Tr::from_key(mnk));
+    const float hif = bad >= 0 ? 0.0f : (float)Tr::to_d(Tr::from_key(mxk));
+    const bool degenerate = bad >= 0 || !(lof < hif);
     if (bad >= 0 && tab.bad_index != nullptr)
-      atomicMin(tab.bad_index, ((unsigned long long)j << 40) | (unsigned long long)(off + bad));
-    const double span = __dsub_rn(hi, lo), pitch = __ddiv_rn(1.0, top);
+      atomicMin(tab.bad_index, ((unsigned long long)br.j << 40) | (unsigned long long)(br.off + bad));
+    const double lo = lof;
+    const double span = __dsub_rn((double)hif, lo), pitch = __ddiv_rn(1.0, top);
     U128 st{0, 0}, inc{0, 0};
     double r = 0.0;
     float shift_f = 0.0f;
     if (!degenerate) {
-      seed_bucket(J.seed, (uint64_t)(J.global_start + off), st, inc);
+      seed_bucket(J.seed, (uint64_t)(J.global_start + br.off), st, inc);
       if (INNER == 0) {
         st = mad128(st, pcg_mult(), inc);
         const double d = u64_to_unit_double(pcg_output(st));
@@ -453,11 +694,11 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
     }
     uint64_t acc = 0;
     int nacc = 0;
-    int64_t o = lb * pbs;
+    int64_t o = br.lb * pbs;
     for (int i = 0; i < n; ++i) {
       uint32_t code = 0;
       if (!degenerate) {
-        const double a = __dsub_rn(InTraits<T>::to_d(x[i]), lo);
+        const double a = __dsub_rn(Tr::to_d(x[i]), lo);
         if (INNER == 0) {
           code = exact_shift_code(a, span, r, pitch, top);
         } else {
@@ -468,34 +709,24 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
       acc |= (uint64_t)code << nacc;
       nacc += bits;
       while (nacc >= 8) {
-        for (int d = 0; d < J.ndst; ++d) J.codes[d][o] = (uint8_t)acc;
-        ++o;
+        J.codes[o++] = (uint8_t)acc;
         acc >>= 8;
         nacc -= 8;
       }
     }
-    if (nacc > 0)
-      for (int d = 0; d < J.ndst; ++d) J.codes[d][o] = (uint8_t)acc;
-    for (int d = 0; d < J.ndst; ++d) {
-      float* m = J.meta[d] + 3 * lb;
-      m[0] = degenerate ? 0.0f : shift_f;
-      m[1] = bad >= 0 ? 0.0f : lof;
-      m[2] = bad >= 0 ? 0.0f : hif;
-    }
+    if (nacc > 0) J.codes[o] = (uint8_t)acc;
+    float* m = J.meta + 3 * br.lb;
+    m[0] = degenerate ? 0.0f : shift_f;
+    m[1] = lof;
+    m[2] = hif;
   }
 }
 
 // ---------------------------------------------------------------------------
 // K3 / K4: dequantize (one source) or ordered dequantize-accumulate (P sources).
 // ---------------------------------------------------------------------------
-// Bits [4*bits*gi, 4*bits*(gi+1)) of a bucket payload of pbytes bytes.
-__device__ __forceinline__ uint64_t load_group_bits(const uint8_t* p, int gi, int bits, int64_t pbytes, bool full) {
-  if (full) {
-    if (bits == 8) return *reinterpret_cast<const uint32_t*>(p + 4 * (int64_t)gi);
-    if (bits == 4) return *reinterpret_cast<const uint16_t*>(p + 2 * (int64_t)gi);
-    if (bits == 16) return *reinterpret_cast<const unsigned long long*>(p + 8 * (int64_t)gi);
-    if (bits == 2) return p[gi];
-  }
+// Bits [4*bits*gi, 4*bits*(gi+1)) of a bucket payload of pbytes bytes (any width).
+__device__ __forceinline__ uint64_t load_group_bits_any(const uint8_t* p, int gi, int bits, int64_t pbytes) {
   const int64_t bitoff = (int64_t)gi * 4 * bits;
   const int64_t b0 = bitoff >> 3;
   const int sh = (int)(bitoff & 7);
@@ -505,6 +736,14 @@ __device__ __forceinline__ uint64_t load_group_bits(const uint8_t* p, int gi, in
     if (b0 + k < pbytes) acc |= (unsigned __int128)p[b0 + k] << (8 * k);
   const uint64_t v = (uint64_t)(acc >> sh);
   return bits == 16 ? v : (v & ((1ull << (4 * bits)) - 1ull));
+}
+
+template <int BITS>
+__device__ __forceinline__ uint64_t load_group_direct(const uint8_t* __restrict__ p, int gi) {
+  if (BITS == 8) return __ldg(reinterpret_cast<const uint32_t*>(p) + gi);
+  if (BITS == 4) return __ldg(reinterpret_cast<const uint16_t*>(p) + gi);
+  if (BITS == 16) return __ldg(reinterpret_cast<const unsigned long long*>(p) + gi);
+  return __ldg(p + gi);
 }
 
 __device__ __forceinline__ double code_to_double(uint32_t c) {
@@ -552,9 +791,11 @@ __device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, c
 // starting from +0.0, then divided by `divisor` (acc = zeros; acc = acc + vals;
 // acc / P -- sharded.py:385-431).  Per-source scales of the current bucket are
 // staged in shared memory (one row per team) by lanes 0..nsrc-1.
-template <int TL, int OUT, bool VEC, bool ACC>
+// BITS > 0: direct width with aligned group loads on full buckets; BITS == 0: any width.
+template <int BITS, int TL, int OUT, bool VEC, bool ACC>
 __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJobTable tab) {
   constexpr int TEAMS = 32 / TL;
+  constexpr int U = 4;  // groups whose code words are loaded before use
   __shared__ double sm_meta[ACC ? 8 : 1][ACC ? TEAMS : 1][8][3];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -562,12 +803,14 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
   const int team = lane / TL;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int S = tab.bucket, bits = tab.bits;
+  const int S = tab.bucket;
+  const int bits = BITS > 0 ? BITS : tab.bits;
   const double top = (double)((1u << bits) - 1u);
   const int64_t pbs = payload_bytes(S, bits);
   const int groups = (S + 3) / 4;
   const int gl = (groups + TL - 1) / TL;
   const uint64_t cmask = (1ull << bits) - 1ull;
+  const bool cvec = BITS > 0 && tab.codes_vec;
 
   for (int64_t b0 = warp * TEAMS; b0 < tab.total_buckets; b0 += nwarps * TEAMS) {
     const int64_t b = b0 + team;
@@ -586,20 +829,43 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
         lo = (double)m[1];
         pitch = __ddiv_rn(__dsub_rn((double)m[2], lo), top);  // QuantizedBlock.pitch
       }
-      const uint8_t* cp = J.codes[0] + lb * pbs;
-      for (int g = 0; g < gl; ++g) {
-        const int gi = g * TL + lt;
-        const int e = 4 * gi;
-        if (e >= n) break;
-        const bool full = e + 4 <= n;
-        const uint64_t w = load_group_bits(cp, gi, bits, pb, full && tab.codes_vec);
-        double v[4];
+      const uint8_t* __restrict__ cp = J.codes[0] + lb * pbs;
+      if (cvec && n == S) {
+        for (int g0 = 0; g0 < gl; g0 += U) {
+          uint64_t w[U];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double c = code_to_double((uint32_t)((w >> (i * bits)) & cmask));
-          v[i] = __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift);  // (lo + code*pitch) + shift
+          for (int u = 0; u < U; ++u) {
+            const int gi = (g0 + u) * TL + lt;
+            w[u] = (g0 + u < gl && 4 * gi < n) ? load_group_direct<BITS>(cp, gi) : 0ull;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int gi = (g0 + u) * TL + lt;
+            if (g0 + u < gl && 4 * gi < n) {
+              double v[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const double c = code_to_double((uint32_t)((w[u] >> (i * bits)) & cmask));
+                v[i] = __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift);  // (lo + code*pitch) + shift
+              }
+              store_out4<OUT, VEC>(J.out, off + 4 * gi, 4, v);
+            }
+          }
         }
-        store_out4<OUT, VEC>(J.out, off + e, n - e, v);
+      } else {
+        for (int g = 0; g < gl; ++g) {
+          const int gi = g * TL + lt;
+          const int e = 4 * gi;
+          if (e >= n) break;
+          const uint64_t w = load_group_bits_any(cp, gi, bits, pb);
+          double v[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double c = code_to_double((uint32_t)((w >> (i * bits)) & cmask));
+            v[i] = __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift);
+          }
+          store_out4<OUT, VEC>(J.out, off + e, n - e, v);
+        }
       }
     } else {
       const int nsrc = J.nsrc;
@@ -617,14 +883,24 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
         const int e = 4 * gi;
         if (e >= n) break;
         const bool full = e + 4 <= n;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int p = 0; p < nsrc; ++p) {
-          const double lo = row[p][0], pitch = row[p][1], shift = row[p][2];
-          const uint64_t w = load_group_bits(J.codes[p] + lb * pbs, gi, bits, pb, full && tab.codes_vec);
+        uint64_t w[8];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const double c = code_to_double((uint32_t)((w >> (i * bits)) & cmask));
-            acc[i] = __dadd_rn(acc[i], __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift));
+        for (int p = 0; p < 8; ++p) {
+          if (p < nsrc) {
+            const uint8_t* __restrict__ cp = J.codes[p] + lb * pbs;
+            w[p] = (cvec && full) ? load_group_direct<BITS>(cp, gi) : load_group_bits_any(cp, gi, bits, pb);
+          }
+        }
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          if (p < nsrc) {
+            const double lo = row[p][0], pitch = row[p][1], shift = row[p][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const double c = code_to_double((uint32_t)((w[p] >> (i * bits)) & cmask));
+              acc[i] = __dadd_rn(acc[i], __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift));
+            }
           }
         }
         if (tab.divisor != 1) {
@@ -648,18 +924,45 @@ inline int team_lanes(int S) {
   return tl;
 }
 
-inline int grid_for(int64_t total_buckets, int teams_per_warp, int sms) {
+inline int grid_for(int64_t total_buckets, int teams_per_warp, int sms, int warps_per_cta = 8, int ctas_per_sm = 8) {
   const int64_t warps = (total_buckets + teams_per_warp - 1) / teams_per_warp;
-  const int64_t blocks = (warps + 7) / 8;
-  const int64_t cap = (int64_t)sms * 8;  // 8 resident 256-thread CTAs per SM at most
+  const int64_t blocks = (warps + warps_per_cta - 1) / warps_per_cta;
+  const int64_t cap = (int64_t)sms * ctas_per_sm;
   return (int)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
+// Fast TMA path.  Returns false when the configuration needs the general kernel.
+template <typename T, int INNER, int BITS, int TL>
+cudaError_t launch_q_tma(const QJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  constexpr int NST = 2;
+  constexpr int TEAMS = 32 / TL;
+  const size_t stage = (size_t)TEAMS * tab.bucket * sizeof(T);
+  int wpc = 8;
+  while (wpc > 1 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
+  const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t);
+  auto kern = quantize_tma_kernel<T, INNER, BITS, TL, NST>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm = (int)((200 * 1024) / smem) < 1 ? 1 : (int)((200 * 1024) / smem);
+  const int grid = grid_for(tab.total_buckets, TEAMS, sms, wpc, per_sm < 8 ? per_sm : 8);
+  kern<<<grid, wpc * 32, smem, s>>>(tab, vec ? 1 : 0);
+  return cudaGetLastError();
 }
 
 template <typename T, int INNER, int TL>
 cudaError_t launch_q_tl(const QJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  const int S = tab.bucket;
+  if (S * (int)sizeof(T) <= 8192) {
+    switch (tab.bits) {
+      case 8: return launch_q_tma<T, INNER, 8, TL>(tab, vec, sms, s);
+      case 4: return launch_q_tma<T, INNER, 4, TL>(tab, vec, sms, s);
+      case 2: return launch_q_tma<T, INNER, 2, TL>(tab, vec, sms, s);
+      case 16: return launch_q_tma<T, INNER, 16, TL>(tab, vec, sms, s);
+      default: break;
+    }
+  }
   // TL < 32 only when the bucket has <= TL groups of 4: one group per lane.
   constexpr int G = TL == 32 ? 8 : 1;
-  const int S = tab.bucket;
   const int gl = ((S + 3) / 4 + TL - 1) / TL;
   const int grid = grid_for(tab.total_buckets, 32 / TL, sms);
   if (TL < 32 || gl <= G) {

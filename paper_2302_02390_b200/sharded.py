@@ -257,6 +257,8 @@ class QSDPHooks:
                     if p != q:
                         entry.record(Transfer("reducescatter", layer.name, width, (e - s) * width // 8, 1,
                                               (e - s) * width))
-                outs.append(acc / P)
+                # tensor/tensor true division (torch turns `/ python_scalar` into a
+                # reciprocal multiply on CUDA, which is not the reference's acc / P)
+                outs.append(torch.div(acc, torch.full_like(acc, float(P))))
         entry.reducescatter_events += 1
         return [o.cpu().numpy() for o in outs]

@@ -1,0 +1,54 @@
+"""Run each hot-path kernel on a GPT-2-small-sized bucket set (for ncu / timing).
+
+    python scripts/prof_kernels.py [--n ELEMS] [--reps R]
+Launch order per rep: K1 (shift quantize), K3 (dequantize), K2 (stochastic
+quantize), K4 (dequant-accumulate, P=1).  Prints CUDA-event GB/s per kernel.
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2302_02390_b200.quantize import (QuantSpec, SegmentKey, codes_bytes, dequant_accumulate,  # noqa: E402
+                                            dequantize_segments, num_buckets, quantize_segments)
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=38633472)  # wte + wpe of GPT-2 small
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--bits", type=int, default=8)
+ap.add_argument("--gbits", type=int, default=8)
+ap.add_argument("--bucket", type=int, default=1024)
+a = ap.parse_args()
+dev = torch.device("cuda", 0)
+n = a.n
+x = torch.randn(n, device=dev) * 0.02
+g = torch.randn(n, device=dev) * 1e-3
+out = torch.empty(n, device=dev)
+ws, gs = QuantSpec(a.bits, a.bucket, "shift"), QuantSpec(a.gbits, a.bucket, "uniform_stochastic")
+wq = (torch.empty(codes_bytes(n, ws) + 16, dtype=torch.uint8, device=dev),
+      torch.empty((num_buckets(n, a.bucket), 3), device=dev))
+gq = (torch.empty(codes_bytes(n, gs) + 16, dtype=torch.uint8, device=dev),
+      torch.empty((num_buckets(n, a.bucket), 3), device=dev))
+cbw = codes_bytes(n, ws) + 12 * num_buckets(n, a.bucket)
+cbg = codes_bytes(n, gs) + 12 * num_buckets(n, a.bucket)
+kern = {
+    "K1": (lambda s: quantize_segments([(x, 0, SegmentKey(0, s, 0, 0, 0))], ws, out=[wq]), 4 * n + cbw),
+    "K3": (lambda s: dequantize_segments([(wq[0], wq[1], n, out)], ws), cbw + 4 * n),
+    "K2": (lambda s: quantize_segments([(g, 0, SegmentKey(0, s, 0, 2, 0))], gs, out=[gq]), 4 * n + cbg),
+    "K4": (lambda s: dequant_accumulate([gq], n, gs, 1, out=out), cbg + 4 * n),
+}
+res = {k: 0.0 for k in kern}
+for r in range(a.reps):
+    for k, (fn, nb) in kern.items():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn(r)
+        e1.record()
+        torch.cuda.synchronize()
+        if r > 0:
+            res[k] += e0.elapsed_time(e1)
+for k, (fn, nb) in kern.items():
+    t = res[k] / max(1, a.reps - 1)
+    print(f"{k}: {t:.4f} ms  {nb / t / 1e6:.1f} GB/s")
