@@ -4,9 +4,11 @@
 namespace qsdp {
 template <int BITS, int TL, int OUT, bool ACC>
 static cudaError_t launch_d_tl(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
-  const int grid = grid_for(tab.total_buckets, 32 / TL, sms);
-  if (vec) dequant_kernel<BITS, TL, OUT, true, ACC><<<grid, 256, 0, s>>>(tab);
-  else dequant_kernel<BITS, TL, OUT, false, ACC><<<grid, 256, 0, s>>>(tab);
+  auto go = [&](auto kern) {
+    kern<<<persistent_grid(kern, 256, 0, tab.total_buckets, 32 / TL, sms), 256, 0, s>>>(tab);
+  };
+  if (vec) go(dequant_kernel<BITS, TL, OUT, true, ACC>);
+  else go(dequant_kernel<BITS, TL, OUT, false, ACC>);
   return cudaGetLastError();
 }
 

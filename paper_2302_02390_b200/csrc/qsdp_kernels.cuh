@@ -509,6 +509,300 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
 }
 
 // ---------------------------------------------------------------------------
+// K1/K2 hot path for buckets of >= 128 elements (one warp per bucket).
+// Same pipeline as quantize_tma_kernel, plus:
+//  * per-bucket PCG64 seeding done lane-parallel, 32 future buckets at a time
+//    (lane L seeds the warp's bucket k0+L), broadcast with shuffles;
+//  * division-free certified codes with the fp64 chain folded into one DFMA:
+//      shift:  y = (v-lo)*K1 + C,  K1 = fl(fl(1/span)*top),  C = fl(M+1/2 - fl(r*top))
+//              -> code = clamp(floor(y - M), 0, top)  (the +1/2 makes floor == rint)
+//      stoch:  y = (v-lo)*K1 + M  -> s in 32.32 fixed point: ip, fq
+//              code = ip + (fq > d_hi)  with d_hi = top 32 bits of the draw
+//    y's 32.32 fixed-point error is < 1.3 units of 2^-32, so a
+//    code is certain unless (shift) |frac - 1/2| <= 2 units, or (stoch)
+//    fq in {d_hi, d_hi+1} or fq == 0 off the bucket's extrema; those elements
+//    are recomputed with the exact __ddiv_rn chain.
+// ---------------------------------------------------------------------------
+// Partial / unaligned / degenerate bucket (one per segment at most on the hot
+// path): per-lane seeding and the Coder path; out of line to keep the fast
+// loop's register budget.  Returns the bucket's f32 shift.
+template <typename T, int INNER, int BITS>
+static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix& seed, uint64_t start, const T* x, int n,
+                                                             int gl, uint8_t* cbase, float lof, float hif,
+                                                             bool degenerate, int lane) {
+  Coder<T, INNER> cd;
+  float shift_f = 0.0f;
+  if (!degenerate) cd.setup(lof, hif, BITS, seed, start, lane, 32, shift_f);
+  const int64_t pb = payload_bytes(n, BITS);
+  for (int g = 0; g < gl; ++g) {
+    const int gi = g * 32 + lane;
+    const int e = 4 * gi;
+    if (e < n) {
+      uint64_t w = 0;
+      if (!degenerate) {
+        T v[4];
+        load_group<T, false, false>(x, e, n, v);
+        w = cd.group(v, e, n, BITS);
+      }
+      store_direct<BITS>(cbase, gi, w, pb, e + 4 <= n);
+    }
+  }
+  return shift_f;
+}
+
+constexpr double kMagic = 1572864.0;  // 1.5 * 2^20
+
+struct SeedOut {
+  U128 s0, inc;
+  double r;
+};
+
+template <int INNER>
+__device__ __forceinline__ SeedOut seed_for(const QJobTable& tab, int64_t b, int S, double pitch) {
+  SeedOut o;
+  o.r = 0.0;
+  o.s0 = U128{0, 0};
+  o.inc = U128{0, 0};
+  if (b < tab.total_buckets) {
+    const BucketRef br = resolve_q(tab, b, S);
+    const QJob& J = tab.jobs[br.j];
+    seed_bucket(J.seed, (uint64_t)(J.global_start + br.off), o.s0, o.inc);
+    if (INNER == 0) {
+      const U128 s1 = mad128(o.s0, pcg_mult(), o.inc);
+      const double d = u64_to_unit_double(pcg_output(s1));
+      o.r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));  // uniform(-p/2, p/2)
+    }
+  }
+  return o;
+}
+
+__device__ __forceinline__ U128 shfl_u128(const U128& v, int src) {
+  U128 r;
+  r.lo = __shfl_sync(0xffffffffu, v.lo, src);
+  r.hi = __shfl_sync(0xffffffffu, v.hi, src);
+  return r;
+}
+
+// Cached job lookup: a warp walks buckets in increasing order, so the job
+// index only moves forward; re-scan only when the bucket leaves the cached job.
+struct JobCursor {
+  int j = 0;
+  int64_t lo = 0, hi = -1;  // bucket range [lo, hi) of job j
+  __device__ __forceinline__ BucketRef get(const QJobTable& tab, int64_t b, int S) {
+    if (b < lo || b >= hi) {
+      j = find_job_q(tab, b);
+      lo = tab.jobs[j].bucket_base;
+      hi = j + 1 < tab.njobs ? tab.jobs[j + 1].bucket_base : tab.total_buckets;
+    }
+    BucketRef r;
+    r.j = j;
+    r.lb = b - lo;
+    r.off = r.lb * S;
+    r.n = (int)min((int64_t)S, tab.jobs[j].length - r.off);
+    return r;
+  }
+};
+
+template <typename T, int INNER, int BITS, int NST>
+__global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_constant__ QJobTable tab) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  using Tr = InTraits<T>;
+  using K = typename Tr::Key;
+  constexpr uint32_t TOP = (1u << BITS) - 1u;
+  const int S = tab.bucket;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int wpc = blockDim.x >> 5;
+  T* wbuf = reinterpret_cast<T*>(smem) + (int64_t)wib * NST * S;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)wpc * NST * S * sizeof(T)) + wib * NST;
+  const int64_t gw = (int64_t)blockIdx.x * wpc + wib;
+  const int64_t nw = (int64_t)gridDim.x * wpc;
+  const int64_t total = tab.total_buckets;
+  const int64_t pbs = payload_bytes(S, BITS);
+  const int gl = (S / 4 + 31) / 32;
+  const double top = (double)TOP;
+  const double pitch = __ddiv_rn(1.0, top);
+
+  // per-lane jump constants: lane starts at element 4*lane, groups are 128 apart
+  U128 A0{1, 0}, G0{0, 0}, JA{1, 0}, JG{0, 0};
+  if (INNER == 1) {
+    const JumpEntry e0 = g_jump[4 * lane + 1];
+    const JumpEntry ej = g_jump[4 * 32 - 3];
+    A0 = e0.a; G0 = e0.g; JA = ej.a; JG = ej.g;
+  }
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  auto bucket_of = [&](int64_t k) { return gw + k * nw; };
+  JobCursor icur, mcur;
+  auto issue = [&](int64_t k) {
+    if (lane == 0) {
+      const int64_t b = bucket_of(k);
+      uint64_t* bar = &bars[k % NST];
+      uint32_t bytes = 0;
+      const T* src = nullptr;
+      const BucketRef br = icur.get(tab, b, S);
+      if (br.n == S) {
+        src = reinterpret_cast<const T*>(tab.jobs[br.j].x) + br.off;
+        if (((uintptr_t)src & 15u) == 0) bytes = (uint32_t)(S * sizeof(T));
+      }
+      mbar_arrive_tx(bar, bytes);
+      if (bytes) tma_load_1d(wbuf + (k % NST) * S, src, bytes, bar);
+    }
+  };
+  for (int64_t k = 0; k < NST; ++k)
+    if (bucket_of(k) < total) issue(k);
+
+  SeedOut seeds{};
+  for (int64_t k = 0; bucket_of(k) < total; ++k) {
+    if ((k & 31) == 0) seeds = seed_for<INNER>(tab, bucket_of(k + lane), S, pitch);
+    const int stage = (int)(k % NST);
+    const int64_t b = bucket_of(k);
+    const BucketRef br = mcur.get(tab, b, S);
+    const QJob& J = tab.jobs[br.j];
+    const int n = br.n;
+    const T* gx = reinterpret_cast<const T*>(J.x) + br.off;
+    const bool in_smem = n == S && (((uintptr_t)gx & 15u) == 0);
+    const T* sb = wbuf + stage * S;
+    mbar_wait(&bars[stage], (uint32_t)((k / NST) & 1));
+
+    // ---- pass 1: min/max keys (quantize.py:251-252) --------------------------
+    K mnk = Tr::kMax, mxk = Tr::kMin;
+    if (in_smem) {
+#pragma unroll 4
+      for (int g = 0; g < gl; ++g) {
+        const int e = 4 * (g * 32 + lane);
+        if (e < n) {
+          T v[4];
+          lds_group(sb, e, v);
+          const K k0 = Tr::key(v[0]), k1 = Tr::key(v[1]), k2 = Tr::key(v[2]), k3 = Tr::key(v[3]);
+          mnk = min(min(mnk, k0), min(k1, min(k2, k3)));
+          mxk = max(max(mxk, k0), max(k1, max(k2, k3)));
+        }
+      }
+    } else {
+      for (int g = 0; g < gl; ++g) {
+        const int e = 4 * (g * 32 + lane);
+        if (e < n) {
+          T v[4];
+          load_group<T, false, false>(gx, e, n, v);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (e + i < n) {
+              mnk = min(mnk, Tr::key(v[i]));
+              mxk = max(mxk, Tr::key(v[i]));
+            }
+        }
+      }
+    }
+    mnk = team_min_k<32>(mnk);
+    mxk = team_max_k<32>(mxk);
+    const bool nonfinite = n > 0 && !(Tr::kNegInf < mnk && mxk < Tr::kPosInf);
+    const T mnv = Tr::from_key(mnk), mxv = Tr::from_key(mxk);
+    const float lof = nonfinite ? 0.0f : (float)Tr::to_d(mnv);
+    const float hif = nonfinite ? 0.0f : (float)Tr::to_d(mxv);
+    const bool degenerate = nonfinite || !(lof < hif);  // quantize.py:254-264
+    if (nonfinite && lane == 0 && tab.bad_index != nullptr) {
+      const int i = first_nonfinite<T>(in_smem ? sb : gx, n);
+      atomicMin(tab.bad_index, ((unsigned long long)br.j << 40) | (unsigned long long)(br.off + i));
+    }
+
+    // ---- pass 2: codes --------------------------------------------------------
+    const int src_lane = (int)(k & 31);
+    const double r = __shfl_sync(0xffffffffu, seeds.r, src_lane);
+    const U128 s0 = INNER == 1 ? shfl_u128(seeds.s0, src_lane) : U128{0, 0};
+    const U128 inc = INNER == 1 ? shfl_u128(seeds.inc, src_lane) : U128{0, 0};
+    uint8_t* cbase = J.codes + br.lb * pbs;
+    const double lo = (double)lof;
+    const double span = __dsub_rn((double)hif, lo);
+    float shift_f = 0.0f;
+    if (!degenerate && in_smem) {
+      const double inv = __drcp_rn(span);
+      const double K1 = __dmul_rn(inv, top);
+      if (INNER == 0) {
+        shift_f = __double2float_rn(__dmul_rn(r, span));  // _f32(r*(hi-lo))
+        const double C = __dsub_rn(kMagic + 0.5, __dmul_rn(r, top));
+#pragma unroll 2
+        for (int g = 0; g < gl; ++g) {
+          const int gi = g * 32 + lane;
+          const int e = 4 * gi;
+          if (e < n) {
+            T v[4];
+            lds_group(sb, e, v);
+            uint32_t c[4];
+            bool unc = false;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              double a = __dsub_rn(Tr::to_d(v[i]), lo);
+              if constexpr (sizeof(T) == 8) a = fmin(fmax(a, 0.0), span);  // == np.clip of u
+              const double y = __fma_rn(a, K1, C);
+              const uint32_t fr = (uint32_t)__double2loint(y);
+              const int ip = (int)((uint32_t)__double2hiint(y) & 0xFFFFFu) - (1 << 19);
+              unc |= (fr + 2u) <= 4u;  // |frac - 1/2| <= 2 units: not certified
+              c[i] = (uint32_t)min(max(ip, 0), (int)TOP);
+            }
+            if (unc) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                c[i] = exact_shift_code(__dsub_rn(Tr::to_d(v[i]), lo), span, r, pitch, top);
+            }
+            const uint64_t w = (uint64_t)c[0] | ((uint64_t)c[1] << BITS) | ((uint64_t)c[2] << (2 * BITS)) |
+                               ((uint64_t)c[3] << (3 * BITS));
+            store_direct<BITS>(cbase, gi, w, 0, true);
+          }
+        }
+      } else {
+        U128 st = add128(mul128(A0, s0), mul128(G0, inc));  // state_{4*lane+1}
+        const U128 jc = mul128(JG, inc);
+#pragma unroll 2
+        for (int g = 0; g < gl; ++g) {
+          const int gi = g * 32 + lane;
+          const int e = 4 * gi;
+          if (e < n) {
+            T v[4];
+            lds_group(sb, e, v);
+            uint64_t w = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              double a = __dsub_rn(Tr::to_d(v[i]), lo);
+              if constexpr (sizeof(T) == 8) a = fmin(fmax(a, 0.0), span);
+              const double y = __fma_rn(a, K1, kMagic);
+              const uint32_t fq = (uint32_t)__double2loint(y);
+              const uint32_t ip = (uint32_t)__double2hiint(y) & 0x7FFFFu;  // s >= 0: drop the 2^19 offset bit
+              const uint32_t dh = pcg_output_hi32(st);
+              uint32_t c = ip + (fq > dh ? 1u : 0u);
+              const bool unc = (fq - dh) <= 1u || (fq == 0u && v[i] != mnv && v[i] != mxv);
+              if (unc) c = exact_stoch_code(__dsub_rn(Tr::to_d(v[i]), lo), span, top, st);
+              w |= (uint64_t)c << (i * BITS);
+              if (i < 3) st = mad128(st, pcg_mult(), inc);
+            }
+            st = add128(mul128(JA, st), jc);
+            store_direct<BITS>(cbase, gi, w, 0, true);
+          }
+        }
+      }
+    } else if (n > 0) {
+      shift_f = quantize_bucket_general<T, INNER, BITS>(J.seed, (uint64_t)(J.global_start + br.off), in_smem ? sb : gx,
+                                                        n, gl, cbase, lof, hif, degenerate, lane);
+    }
+    if (lane == 0) {
+      float* m = J.meta + 3 * br.lb;
+      m[0] = degenerate ? 0.0f : shift_f;
+      m[1] = lof;
+      m[2] = hif;
+    }
+    __syncwarp();
+    fence_proxy_async();
+    if (bucket_of(k + NST) < total) issue(k + NST);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1/K2 for any width 1..16 (odd widths merge lane pairs into whole bytes),
 // S % 8 == 0.  Registers hold up to G groups per lane (HOLD) or the bucket is
 // re-read (second pass through L1/L2).
@@ -795,7 +1089,7 @@ __device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, c
 template <int BITS, int TL, int OUT, bool VEC, bool ACC>
 __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJobTable tab) {
   constexpr int TEAMS = 32 / TL;
-  constexpr int U = 4;  // groups whose code words are loaded before use
+  constexpr int U = 8;  // groups whose code words are loaded before use
   __shared__ double sm_meta[ACC ? 8 : 1][ACC ? TEAMS : 1][8][3];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -931,22 +1225,52 @@ inline int grid_for(int64_t total_buckets, int teams_per_warp, int sms, int warp
   return (int)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
 }
 
+// Persistent grid: exactly the CTAs that are co-resident (one wave), fewer if
+// the work is smaller.  Every kernel grid-strides over buckets, so a partial
+// second wave would only add a tail.
+template <typename F>
+inline int persistent_grid(F kern, int threads, size_t smem, int64_t total_buckets, int teams_per_warp, int sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return grid_for(total_buckets, teams_per_warp, sms, threads / 32, per_sm);
+}
+
 // Fast TMA path.  Returns false when the configuration needs the general kernel.
-template <typename T, int INNER, int BITS, int TL>
-cudaError_t launch_q_tma(const QJobTable& tab, bool vec, int sms, cudaStream_t s) {
+template <typename T, int INNER, int BITS>
+cudaError_t launch_q_tma32(const QJobTable& tab, int sms, cudaStream_t s) {
   constexpr int NST = 2;
-  constexpr int TEAMS = 32 / TL;
-  const size_t stage = (size_t)TEAMS * tab.bucket * sizeof(T);
+  const size_t stage = (size_t)tab.bucket * sizeof(T);
   int wpc = 8;
-  while (wpc > 1 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
+  while (wpc > 2 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
   const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t);
-  auto kern = quantize_tma_kernel<T, INNER, BITS, TL, NST>;
+  auto kern = quantize_tma32_kernel<T, INNER, BITS, NST>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int per_sm = (int)((200 * 1024) / smem) < 1 ? 1 : (int)((200 * 1024) / smem);
-  const int grid = grid_for(tab.total_buckets, TEAMS, sms, wpc, per_sm < 8 ? per_sm : 8);
-  kern<<<grid, wpc * 32, smem, s>>>(tab, vec ? 1 : 0);
+  const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, 1, sms);
+  kern<<<grid, wpc * 32, smem, s>>>(tab);
   return cudaGetLastError();
+}
+
+template <typename T, int INNER, int BITS, int TL>
+cudaError_t launch_q_tma(const QJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  if constexpr (TL == 32) {
+    (void)vec;
+    return launch_q_tma32<T, INNER, BITS>(tab, sms, s);
+  } else {
+    constexpr int NST = 2;
+    constexpr int TEAMS = 32 / TL;
+    const size_t stage = (size_t)TEAMS * tab.bucket * sizeof(T);
+    int wpc = 8;
+    while (wpc > 1 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
+    const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t);
+    auto kern = quantize_tma_kernel<T, INNER, BITS, TL, NST>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, TEAMS, sms);
+    kern<<<grid, wpc * 32, smem, s>>>(tab, vec ? 1 : 0);
+    return cudaGetLastError();
+  }
 }
 
 template <typename T, int INNER, int TL>
@@ -964,13 +1288,15 @@ cudaError_t launch_q_tl(const QJobTable& tab, bool vec, int sms, cudaStream_t s)
   // TL < 32 only when the bucket has <= TL groups of 4: one group per lane.
   constexpr int G = TL == 32 ? 8 : 1;
   const int gl = ((S + 3) / 4 + TL - 1) / TL;
-  const int grid = grid_for(tab.total_buckets, 32 / TL, sms);
+  auto go = [&](auto kern) {
+    kern<<<persistent_grid(kern, 256, 0, tab.total_buckets, 32 / TL, sms), 256, 0, s>>>(tab);
+  };
   if (TL < 32 || gl <= G) {
-    if (vec) quantize_kernel<T, INNER, TL, G, true, true><<<grid, 256, 0, s>>>(tab);
-    else quantize_kernel<T, INNER, TL, G, true, false><<<grid, 256, 0, s>>>(tab);
+    if (vec) go(quantize_kernel<T, INNER, TL, G, true, true>);
+    else go(quantize_kernel<T, INNER, TL, G, true, false>);
   } else if constexpr (TL == 32) {
-    if (vec) quantize_kernel<T, INNER, TL, 1, false, true><<<grid, 256, 0, s>>>(tab);
-    else quantize_kernel<T, INNER, TL, 1, false, false><<<grid, 256, 0, s>>>(tab);
+    if (vec) go(quantize_kernel<T, INNER, TL, 1, false, true>);
+    else go(quantize_kernel<T, INNER, TL, 1, false, false>);
   }
   return cudaGetLastError();
 }

@@ -16,7 +16,7 @@ from paper_2302_02390_b200.quantize import (QuantSpec, SegmentKey, codes_bytes, 
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=38633472)  # wte + wpe of GPT-2 small
-ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--reps", type=int, default=11)
 ap.add_argument("--bits", type=int, default=8)
 ap.add_argument("--gbits", type=int, default=8)
 ap.add_argument("--bucket", type=int, default=1024)
