@@ -39,7 +39,7 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--model", default="gpt2-125m")
@@ -62,7 +62,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -80,6 +80,15 @@ class ClockSampler:
                     pass
 
     def __exit__(self, *a):
+        if not self.samples:  # timed region shorter than the sampling period: take one reading now
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+            except Exception:
+                pass
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -179,15 +188,15 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2302_02390_b200 import _lib
     from paper_2302_02390_b200.comm import QSDPComm, plan_segments
     from paper_2302_02390_b200.gpt import dense_groups
-    from paper_2302_02390_b200.quantize import (QuantSpec, SegmentKey, codes_bytes, dequant_accumulate,
-                                                dequantize_segments, num_buckets, quantize_segments)
+    from paper_2302_02390_b200.quantize import (QuantSpec, SegmentKey, advance_counter, codes_bytes,
+                                                dequant_accumulate, dequantize_segments, num_buckets,
+                                                quantize_segments)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -206,109 +215,120 @@ def main():
     N_total = sum(g.numel for g in groups)
     pad = args.bucket if args.bucket % 8 == 0 else 1
 
-    # ---- synthetic state (device-resident for `value`) ----
+    # ---- synthetic state, resident in HBM for `value` ----
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     state = []
     max_seg = 0
-    for gi, g in enumerate(groups):
+    for g in groups:
         segs = plan_segments(g.numel, world, pad)
         max_seg = max(max_seg, max(n for _, n in segs))
         s, n = segs[rank]
-        shard = torch.randn(max(n, 1), generator=gen, device=dev)[:n].mul_(0.02)
-        grad = torch.randn(g.numel, generator=gen, device=dev).mul_(1e-3)
-        full = torch.empty(g.numel, dtype=out_dt, device=dev)
-        gshard = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
-        wq = (torch.empty(codes_bytes(g.numel, wspec) + 16, dtype=torch.uint8, device=dev),
-              torch.empty((num_buckets(g.numel, args.bucket), 3), dtype=torch.float32, device=dev))
-        gq = (torch.empty(codes_bytes(g.numel, gspec) + 16, dtype=torch.uint8, device=dev),
-              torch.empty((num_buckets(g.numel, args.bucket), 3), dtype=torch.float32, device=dev))
-        state.append(dict(g=g, segs=segs, shard=shard, grad=grad, full=full, gshard=gshard, wq=wq, gq=gq))
+        st = dict(g=g, segs=segs, n=n)
+        st["shard"] = torch.randn(max(n, 1), generator=gen, device=dev)[:n].mul_(0.02)
+        st["grad"] = torch.randn(g.numel, generator=gen, device=dev).mul_(1e-3)
+        st["full"] = torch.empty(g.numel, dtype=out_dt, device=dev)
+        st["gshard"] = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        st["wq"] = (torch.empty(codes_bytes(g.numel, wspec) + 16, dtype=torch.uint8, device=dev),
+                    torch.empty((num_buckets(g.numel, args.bucket), 3), dtype=torch.float32, device=dev))
+        st["gq"] = (torch.empty(codes_bytes(g.numel, gspec) + 16, dtype=torch.uint8, device=dev),
+                    torch.empty((num_buckets(g.numel, args.bucket), 3), dtype=torch.float32, device=dev))
+        state.append(st)
     flush = torch.empty(64 << 20, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
-
-    comm = QSDPComm(max_seg, wspec, gspec, device=dev) if world > 1 or not args.no_e2e else None
+    step_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+    comm = QSDPComm(max_seg, wspec, gspec, device=dev)
+    comm.set_step_source(step_ctr)
     stream = torch.cuda.current_stream(dev)
 
-    # ---- N=1: batched kernel API with per-kernel CUDA events (same kernels as the comm) ----
+    # ---- the step as a list of launches (kind, bytes, fn) ----
     kinds = ("K1_quantize_shift", "K3_dequantize", "K2_quantize_stochastic", "K4_dequant_accumulate")
-    kbytes = {k: 0 for k in kinds}
-    kev = {k: [] for k in kinds}
-    launches = [0]
 
-    def timed(kind, fn, nbytes, record):
-        if record:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            kev[kind].append((a, b))
-            kbytes[kind] += nbytes
-        else:
-            fn()
-        launches[0] += 1
+    def local_launches():
+        """World 1: the comm's kernels through the batched API (same kernels, per-kernel timing)."""
+        L = []
 
-    def ag_local(st, gi, step, phase, record):
-        n = st["g"].numel
-        res = {}
+        def ag(st, gi, phase):
+            n = st["g"].numel
+            cb = codes_bytes(n, wspec) + 12 * num_buckets(n, args.bucket)
+            L.append((kinds[0], 4 * n + cb, lambda: quantize_segments(
+                [(st["shard"], 0, SegmentKey(0, 0, gi, phase, 0))], wspec, out=[st["wq"]], step_src=step_ctr)))
+            L.append((kinds[1], cb + osz * n, lambda: dequantize_segments(
+                [(st["wq"][0], st["wq"][1], n, st["full"])], wspec, out_dt)))
 
-        def q():
-            res["cm"] = quantize_segments([(st["shard"], 0, SegmentKey(0, step, gi, phase, 0))], wspec,
-                                          out=[st["wq"]])[0]
-        cb = codes_bytes(n, wspec) + 12 * num_buckets(n, args.bucket)
-        timed(kinds[0], q, 4 * n + cb, record)
-        c, m = res["cm"]
-        timed(kinds[1], lambda: dequantize_segments([(c, m, n, st["full"])], wspec, out_dt), cb + osz * n, record)
+        def rs(st, gi):
+            n = st["g"].numel
+            cb = codes_bytes(n, gspec) + 12 * num_buckets(n, args.bucket)
+            L.append((kinds[2], 4 * n + cb, lambda: quantize_segments(
+                [(st["grad"], 0, SegmentKey(0, 0, gi, 2, 0))], gspec, out=[st["gq"]], step_src=step_ctr)))
+            L.append((kinds[3], cb + 4 * n, lambda: dequant_accumulate(
+                [(st["gq"][0], st["gq"][1])], n, gspec, 1, dtype=torch.float32, out=st["gshard"])))
 
-    def rs_local(st, gi, step, record):
-        n = st["g"].numel
-        res = {}
-
-        def q():
-            res["cm"] = quantize_segments([(st["grad"], 0, SegmentKey(0, step, gi, 2, 0))], gspec,
-                                          out=[st["gq"]])[0]
-        cb = codes_bytes(n, gspec) + 12 * num_buckets(n, args.bucket)
-        timed(kinds[2], q, 4 * n + cb, record)
-        timed(kinds[3], lambda: dequant_accumulate([res["cm"]], n, gspec, 1, dtype=torch.float32,
-                                                   out=st["gshard"]), cb + 4 * n, record)
-
-    def step_local(step, record):
         for gi, st in enumerate(state):
-            ag_local(st, gi, step, 0, record)
+            ag(st, gi, 0)
         for gi in range(len(state) - 1, -1, -1):
-            ag_local(state[gi], gi, step, 1, record)
-            rs_local(state[gi], gi, step, record)
+            ag(state[gi], gi, 1)
+            rs(state[gi], gi)
+        return L
 
-    def step_comm(step):
+    def comm_launches():
+        L = []
+        per = 3 if world > 1 else 2  # quantize (+ barrier) + dequant
         for gi, st in enumerate(state):
-            comm.all_gather(st["shard"], st["segs"], SegmentKey(0, step, gi, 0, 0), st["full"])
+            L.append(("AG", per, lambda st=st, gi=gi: comm.all_gather(
+                st["shard"], st["segs"], SegmentKey(0, 0, gi, 0, 0), st["full"])))
         for gi in range(len(state) - 1, -1, -1):
             st = state[gi]
-            comm.all_gather(st["shard"], st["segs"], SegmentKey(0, step, gi, 1, 0), st["full"])
-            comm.reduce_scatter(st["grad"], st["segs"], SegmentKey(0, step, gi, 2, rank), st["gshard"])
-        launches[0] += len(state) * 3 * (3 if world > 1 else 2)
+            L.append(("AG", per, lambda st=st, gi=gi: comm.all_gather(
+                st["shard"], st["segs"], SegmentKey(0, 0, gi, 1, 0), st["full"])))
+            L.append(("RS", per, lambda st=st, gi=gi: comm.reduce_scatter(
+                st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"])))
+        return L
+
+    launches = local_launches() if world == 1 else comm_launches()
+    n_launch = (sum(1 for _ in launches) if world == 1 else sum(x[1] for x in launches)) + 1  # + counter
+
+    def run_step(sel=None):
+        for kind, _, fn in launches:
+            if sel is None or kind == sel:
+                fn()
+        if sel is None:
+            advance_counter(step_ctr)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    run_step = (lambda s, rec: step_local(s, rec)) if world == 1 else (lambda s, rec: step_comm(s))
-    for s in range(args.warmup):
-        run_step(s, False)
-    barrier()
-    launches[0] = 0
-    step_events = []
-    with ClockSampler(local) as clocks:
-        barrier()
-        for s in range(args.steps):
-            flush.fill_(s)  # evict L2 between timed steps (outside the step events)
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
+
+    def time_graph(g, reps, flush_between=True):
+        ev = []
+        for r in range(reps):
+            if flush_between:
+                flush.fill_(r)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            run_step(args.warmup + s, True)
+            g.replay()
             b.record(stream)
-            step_events.append((a, b))
+            ev.append((a, b))
+        return ev
+
+    for _ in range(args.warmup):
+        run_step()
+    barrier()
+    g_step = capture(run_step)
+    for _ in range(args.warmup):  # warm the graph itself
+        g_step.replay()
+    barrier()
+    with ClockSampler(local) as clocks:
         barrier()
-    ms = sum(a.elapsed_time(b) for a, b in step_events)
+        ev = time_graph(g_step, args.steps)
+        barrier()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -316,7 +336,7 @@ def main():
     ms_step = ms / args.steps
     value = world * 12.0 * N_total / (ms_step * 1e-3) / 1e9
 
-    # ---- roofline of the dominant kernel (N=1: per-kernel events inside the timed region) ----
+    # ---- roofline of the dominant kernel: per-kind graphs timed with CUDA events ----
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -324,15 +344,21 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    kernels = {}
-    roofline = None
+    kernels, roofline = {}, None
     if world == 1:
         for k in kinds:
-            tk = sum(a.elapsed_time(b) for a, b in kev[k])
-            if kev[k]:
-                kernels[k] = {"ms_total": round(tk, 4), "launches": len(kev[k]),
-                              "gbs": round(kbytes[k] / (tk * 1e-3) / 1e9, 1), "share": round(tk / ms, 4)}
-        dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
+            nb = sum(x[1] for x in launches if x[0] == k)
+            cnt = sum(1 for x in launches if x[0] == k)
+            gk = capture(lambda k=k: run_step(k))
+            gk.replay()
+            torch.cuda.synchronize(dev)
+            evk = time_graph(gk, args.steps)
+            torch.cuda.synchronize(dev)
+            tk = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+            kernels[k] = {"ms_per_step": round(tk, 4), "launches_per_step": cnt, "avg_launch_us": round(tk / cnt * 1e3, 2),
+                          "gbs": round(nb / (tk * 1e-3) / 1e9, 1), "share_of_step": round(tk / ms_step, 4),
+                          "bytes_per_step": nb}
+        dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
         ach = kernels[dom]["gbs"]
         traffic = None
         try:
@@ -342,42 +368,37 @@ def main():
             pass
         roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                     "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
-                    "bytes_per_launch": round(kbytes[dom] / len(kev[dom]))}
+                    "bytes_per_launch": round(kernels[dom]["bytes_per_step"] / kernels[dom]["launches_per_step"]),
+                    "method": "algorithmic bytes / CUDA-event time of that kernel's launches (graph of one step's "
+                              "launches of the kind, L2 flushed between replays)"}
 
     # ---- e2e: through the C-ABI communicator, host buffers, copies inside the timed region ----
     e2e = None
-    if not args.no_e2e and comm is not None:
+    if not args.no_e2e:
         host = []
         for st in state:
             host.append(dict(shard=st["shard"].cpu().pin_memory(), grad=st["grad"].cpu().pin_memory(),
-                             res=torch.empty_like(st["gshard"], device="cpu").pin_memory()))
+                             res=torch.empty(st["gshard"].numel(), dtype=torch.float32).pin_memory()))
         bi = sum(h["shard"].numel() * 4 + h["grad"].numel() * 4 for h in host)
-        bo = sum(st["segs"][rank][1] * 4 for st in state)
+        bo = sum(st["n"] * 4 for st in state)
+        claunch = comm_launches()
 
-        def step_e2e(step):
-            for gi, (st, h) in enumerate(zip(state, host)):
+        def step_e2e():
+            for st, h in zip(state, host):
                 st["shard"].copy_(h["shard"], non_blocking=True)
                 st["grad"].copy_(h["grad"], non_blocking=True)
-            for gi, st in enumerate(state):
-                comm.all_gather(st["shard"], st["segs"], SegmentKey(0, step, gi, 0, 0), st["full"])
-            for gi in range(len(state) - 1, -1, -1):
-                st = state[gi]
-                comm.all_gather(st["shard"], st["segs"], SegmentKey(0, step, gi, 1, 0), st["full"])
-                comm.reduce_scatter(st["grad"], st["segs"], SegmentKey(0, step, gi, 2, rank), st["gshard"])
-                n = st["segs"][rank][1]
-                host[gi]["res"][:n].copy_(st["gshard"][:n], non_blocking=True)
+            for _, _, fn in claunch:
+                fn()
+            for st, h in zip(state, host):
+                h["res"][: st["n"]].copy_(st["gshard"][: st["n"]], non_blocking=True)
+            advance_counter(step_ctr)
 
-        for s in range(max(1, args.warmup)):
-            step_e2e(s)
+        step_e2e()
         barrier()
-        ev = []
-        for s in range(args.steps):
-            flush.fill_(s)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            step_e2e(s)
-            b.record(stream)
-            ev.append((a, b))
+        g_e2e = capture(step_e2e)
+        g_e2e.replay()
+        barrier()
+        ev = time_graph(g_e2e, args.steps)
         barrier()
         ems = sum(a.elapsed_time(b) for a, b in ev)
         if world > 1:
@@ -386,7 +407,8 @@ def main():
             ems = float(t.item())
         e2e = {"value": round(world * 12.0 * N_total / (ems / args.steps * 1e-3) / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "ms_per_step": round(ems / args.steps, 3),
-               "path": "QSDPComm -> qsdp_all_gather / qsdp_reduce_scatter (C ABI), pinned host buffers"}
+               "path": "QSDPComm -> qsdp_all_gather / qsdp_reduce_scatter (C ABI), pinned host buffers, "
+                       "one CUDA graph per step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -402,13 +424,13 @@ def main():
                                    f"AG fwd + AG bwd + RS over {len(groups)} FSDP groups ({N_total} dense params)",
                        "out_dtype": args.out_dtype, "quantizer_input": "f32", "arithmetic": "f64 (bit-exact)",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 126 MB L2",
-                       "parallelism": f"qsdp{world}", "convention": "sum over ranks of 4*N per collective / time"},
+                       "parallelism": f"qsdp{world}", "execution": "one CUDA graph per step (device step counter)",
+                       "convention": "sum over ranks of 4*N per collective / time"},
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches[0], "clocks": clocks.summary(),
+            "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
-    if comm is not None:
-        comm.close()
+    comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

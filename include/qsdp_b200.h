@@ -123,6 +123,13 @@ qsdp_status qsdp_quantize(const void* x, int32_t x_dtype, qsdp_segment seg, cons
                           void* stream);
 qsdp_status qsdp_quantize_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
                                 const qsdp_qcfg* cfg, uint64_t* d_bad, void* stream);
+/* Same, with the keys' step offset read on the device at run time
+ * (step = key.step + *d_step): a captured CUDA graph replays with fresh noise. */
+qsdp_status qsdp_quantize_batch_dstep(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
+                                      const qsdp_qcfg* cfg, uint64_t* d_bad, const uint64_t* d_step,
+                                      void* stream);
+/* *d_counter += delta on the stream (advances a device step counter inside a graph). */
+qsdp_status qsdp_counter_add(uint64_t* d_counter, uint64_t delta, void* stream);
 
 /* ---- K3: dequantize one segment (fp32 out == float32(reference fp64); bf16 == RNE of that) ---- */
 qsdp_status qsdp_dequantize(const uint8_t* codes, const float* meta, int64_t length,
@@ -150,6 +157,10 @@ qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32
                              const qsdp_qcfg* gcfg);
 qsdp_status qsdp_comm_ipc_handle(qsdp_comm* c, void* handle /* QSDP_IPC_HANDLE_BYTES */);
 qsdp_status qsdp_comm_open_peers(qsdp_comm* c, const void* handles /* world*QSDP_IPC_HANDLE_BYTES */);
+/* Keys' step = key.step + *d_step for every later collective (NULL: key.step).
+ * With it, and the communicator's device-side epoch, a sequence of
+ * qsdp_all_gather / qsdp_reduce_scatter calls can be captured in a CUDA graph. */
+qsdp_status qsdp_comm_set_step_source(qsdp_comm* c, const uint64_t* d_step);
 /* Quantized all-gather (ShardedMLP._gather): this rank's shard = segs[rank];
  * every rank writes the dequantized full tensor (sum of segs lengths) to full_out.
  * key->worker is forced to 0 (sharded.py:341). */

@@ -78,6 +78,13 @@ class QSDPComm:
             _lib.check(L.qsdp_comm_open_peers(self._h, cb))
             dist.barrier(group=group)
 
+    def set_step_source(self, counter: torch.Tensor | None) -> None:
+        """Keys use ``key.step + counter`` read on the device (graph replay)."""
+        if counter is not None and (counter.dtype != torch.int64 or counter.device != self.device):
+            raise ValueError("step counter must be an int64 tensor on the communicator's device")
+        self._step_src = counter  # keep alive
+        _lib.check(_lib.lib().qsdp_comm_set_step_source(self._h, counter.data_ptr() if counter is not None else None))
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             _lib.lib().qsdp_comm_destroy(self._h)

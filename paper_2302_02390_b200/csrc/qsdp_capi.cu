@@ -87,25 +87,8 @@ qsdp_status ensure_device(int& sms) {
   return QSDP_OK;
 }
 
-// SeedSequence prefix: absorb root, step, layer, phase, worker (each coerced to
-// LE uint32 words, 0 -> [0]) -- numpy mix_entropy with pool size 4.
-SeedPrefix make_prefix(const qsdp_key& k, uint64_t worker) {
-  uint32_t words[10];
-  int n = 0;
-  const uint64_t f[5] = {k.root_seed, k.step, k.layer, k.phase, worker};
-  for (uint64_t v : f) {
-    words[n++] = (uint32_t)v;
-    if (v >> 32) words[n++] = (uint32_t)(v >> 32);
-  }
-  SeedPrefix p{};
-  uint32_t hc = SS_INIT_A;
-  for (int i = 0; i < 4; ++i) p.pool[i] = ss_hashmix(words[i], hc);
-  for (int s = 0; s < 4; ++s)
-    for (int d = 0; d < 4; ++d)
-      if (s != d) p.pool[d] = ss_mix(p.pool[d], ss_hashmix(p.pool[s], hc));
-  for (int s = 4; s < n; ++s) ss_absorb(p.pool, hc, words[s]);
-  p.hash_const = hc;
-  return p;
+SeedPrefix key_prefix(const qsdp_key& k, uint64_t worker) {
+  return make_prefix(k.root_seed, k.step, k.layer, k.phase, worker);
 }
 
 qsdp_status check_cfg(const qsdp_qcfg* c) {
@@ -129,10 +112,19 @@ struct QJobSpec {
   uint8_t* codes;
   float* meta;
   SeedPrefix seed;
+  uint64_t key[5];
+};
+
+// Device-side sources that make a launch sequence replayable as a CUDA graph.
+struct DynSrc {
+  const unsigned long long* step_ptr = nullptr;    // key step += *step_ptr
+  const unsigned long long* parity_ptr = nullptr;  // slot parity = (*parity_ptr + adj) & 1
+  int64_t parity_stride = 0;
+  int32_t parity_adj = 0;
 };
 
 qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const qsdp_qcfg* cfg,
-                         uint64_t* d_bad, cudaStream_t stream) {
+                         uint64_t* d_bad, cudaStream_t stream, const DynSrc& dyn = DynSrc()) {
   if (x_dtype != QSDP_F32 && x_dtype != QSDP_F64) return fail(QSDP_EINVAL, "input dtype must be f32 or f64");
   int sms = 0;
   qsdp_status st = ensure_device(sms);
@@ -146,6 +138,10 @@ qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const q
     tab.bucket = cfg->bucket;
     tab.inner = cfg->inner;
     tab.bad_index = reinterpret_cast<unsigned long long*>(d_bad);
+    tab.step_ptr = dyn.step_ptr;
+    tab.parity_ptr = dyn.parity_ptr;
+    tab.parity_stride = dyn.parity_stride;
+    tab.parity_adj = dyn.parity_adj;
     int64_t nb = 0;
     bool vec = cfg->bucket % 4 == 0;
     int nj = 0;
@@ -160,6 +156,7 @@ qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const q
       J.global_start = s.global_start;
       J.bucket_base = nb;
       J.seed = s.seed;
+      for (int w = 0; w < 5; ++w) J.key[w] = s.key[w];
       nb += (s.length + cfg->bucket - 1) / cfg->bucket;
       vec = vec && aligned(s.x, 16);
       (void)esz;
@@ -183,7 +180,7 @@ struct DJobSpec {
 };
 
 qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg, int accumulate,
-                        int divisor, int out_dtype, cudaStream_t stream) {
+                        int divisor, int out_dtype, cudaStream_t stream, const DynSrc& dyn = DynSrc()) {
   if (out_dtype != QSDP_F32 && out_dtype != QSDP_F64 && out_dtype != QSDP_BF16)
     return fail(QSDP_EINVAL, "output dtype must be f32, f64 or bf16");
   int sms = 0;
@@ -198,6 +195,9 @@ qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg,
     tab.out_dtype = out_dtype;
     tab.accumulate = accumulate;
     tab.divisor = divisor < 1 ? 1 : divisor;
+    tab.parity_ptr = dyn.parity_ptr;
+    tab.parity_stride = dyn.parity_stride;
+    tab.parity_adj = dyn.parity_adj;
     bool vec = cfg->bucket % 4 == 0;
     bool cvec = cfg->bucket % 8 == 0;
     int64_t nb = 0;
@@ -280,6 +280,12 @@ qsdp_status qsdp_quantize(const void* x, int32_t x_dtype, qsdp_segment seg, cons
 
 qsdp_status qsdp_quantize_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
                                 const qsdp_qcfg* cfg, uint64_t* d_bad, void* stream) {
+  return qsdp_quantize_batch_dstep(items, nitems, x_dtype, cfg, d_bad, nullptr, stream);
+}
+
+qsdp_status qsdp_quantize_batch_dstep(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
+                                      const qsdp_qcfg* cfg, uint64_t* d_bad, const uint64_t* d_step,
+                                      void* stream) {
   qsdp_status st = check_cfg(cfg);
   if (st != QSDP_OK) return st;
   if (nitems < 0 || (nitems > 0 && items == nullptr)) return fail(QSDP_EINVAL, "bad item list");
@@ -299,10 +305,17 @@ qsdp_status qsdp_quantize_batch(const qsdp_qitem* items, int32_t nitems, int32_t
     s.global_start = it.seg.global_start;
     s.codes = it.codes;
     s.meta = it.meta;
-    s.seed = make_prefix(it.key, it.key.worker);
+    s.seed = key_prefix(it.key, it.key.worker);
+    s.key[0] = it.key.root_seed;
+    s.key[1] = it.key.step;
+    s.key[2] = it.key.layer;
+    s.key[3] = it.key.phase;
+    s.key[4] = it.key.worker;
     jobs.push_back(s);
   }
-  return run_quantize(jobs, x_dtype, cfg, d_bad, reinterpret_cast<cudaStream_t>(stream));
+  DynSrc dyn;
+  dyn.step_ptr = reinterpret_cast<const unsigned long long*>(d_step);
+  return run_quantize(jobs, x_dtype, cfg, d_bad, reinterpret_cast<cudaStream_t>(stream), dyn);
 }
 
 qsdp_status qsdp_dequantize(const uint8_t* codes, const float* meta, int64_t length, const qsdp_qcfg* cfg,
@@ -401,24 +414,36 @@ int64_t qsdp_wire_encode(const uint8_t* codes, const float* meta, int64_t length
 // ===========================================================================
 // Multi-GPU communicator (C1 / C2)
 // ===========================================================================
+// Workspace layout (per rank, one cudaMalloc exported over CUDA IPC):
+//   [0, 64)     flags[8]: flags[j] = last epoch rank j signalled to this rank
+//   [128, 136)  epoch: collectives completed (advanced by the barrier kernel)
+//   [256, ...)  slots[2 parities][world]: packed codes (slot_codes) + meta (slot_meta)
+// Every launch reads the epoch on the device, so a whole training step's
+// sequence of collectives can be captured once and replayed as a CUDA graph.
 struct PeerFlags {
   unsigned long long* flags[QSDP_MAX_WORLD];  // flags[j] = base of rank j's flag array
 };
 
-__global__ void qsdp_barrier_kernel(PeerFlags pf, int rank, int world, unsigned long long epoch) {
+constexpr size_t kEpochOff = 128;
+
+__global__ void qsdp_barrier_kernel(PeerFlags pf, int rank, int world, unsigned long long* epoch_ptr) {
   const int t = threadIdx.x;
+  const unsigned long long target = *reinterpret_cast<volatile unsigned long long*>(epoch_ptr) + 1ull;
   if (t < world) {
     __threadfence_system();
-    unsigned long long* dst = pf.flags[t] + rank;  // peer t learns "rank reached epoch"
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
+    unsigned long long* dst = pf.flags[t] + rank;  // peer t learns "rank reached target"
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(target) : "memory");
     const unsigned long long* mine = pf.flags[rank] + t;
     unsigned long long v = 0;
     do {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
-    } while (v < epoch);
+    } while (v < target);
   }
   __syncthreads();
+  if (t == 0) *reinterpret_cast<volatile unsigned long long*>(epoch_ptr) = target;
 }
+
+__global__ void qsdp_counter_add_kernel(unsigned long long* p, unsigned long long delta) { *p += delta; }
 
 struct qsdp_comm {
   int rank = 0, world = 1, device = 0;
@@ -429,17 +454,25 @@ struct qsdp_comm {
   uint8_t* base = nullptr;
   uint8_t* peer[QSDP_MAX_WORLD] = {};
   bool opened[QSDP_MAX_WORLD] = {};
-  unsigned long long epoch = 0;
+  const unsigned long long* step_src = nullptr;
 
   static constexpr size_t kFlagBytes = 256;
-  uint8_t* slot(uint8_t* b, int parity, int idx) const {
-    return b + kFlagBytes + ((size_t)parity * world + idx) * slot_bytes;
-  }
+  uint8_t* slot(uint8_t* b, int idx) const { return b + kFlagBytes + (size_t)idx * slot_bytes; }  // parity 0
+  int64_t parity_stride() const { return (int64_t)world * (int64_t)slot_bytes; }
+  unsigned long long* epoch() const { return reinterpret_cast<unsigned long long*>(base + kEpochOff); }
 };
 
 static size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 extern "C" {
+
+qsdp_status qsdp_counter_add(uint64_t* d_counter, uint64_t delta, void* stream) {
+  if (d_counter == nullptr) return fail(QSDP_EINVAL, "null counter");
+  qsdp_counter_add_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long*>(d_counter), (unsigned long long)delta);
+  QSDP_CUDA(cudaGetLastError());
+  return QSDP_OK;
+}
 
 qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32_t device,
                              int64_t max_segment_elems, const qsdp_qcfg* wcfg, const qsdp_qcfg* gcfg) {
@@ -474,14 +507,20 @@ qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32
     return cuda_fail(e, "cudaMalloc(comm workspace)");
   }
   e = cudaMemset(c->base, 0, c->bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cudaFree(c->base);
     delete c;
     return cuda_fail(e, "cudaMemset(comm workspace)");
   }
   c->peer[rank] = c->base;
-  c->opened[rank] = false;
   *out = c;
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_comm_set_step_source(qsdp_comm* c, const uint64_t* d_step) {
+  if (c == nullptr) return fail(QSDP_EINVAL, "null comm");
+  c->step_src = reinterpret_cast<const unsigned long long*>(d_step);
   return QSDP_OK;
 }
 
@@ -523,14 +562,13 @@ qsdp_status qsdp_comm_destroy(qsdp_comm* c) {
 }
 
 static qsdp_status comm_barrier(qsdp_comm* c, cudaStream_t s) {
-  if (c->world == 1) return QSDP_OK;
   PeerFlags pf;
   memset(&pf, 0, sizeof(pf));
   for (int j = 0; j < c->world; ++j) {
     if (c->peer[j] == nullptr) return fail(QSDP_EPEER, "peers not opened");
     pf.flags[j] = reinterpret_cast<unsigned long long*>(c->peer[j]);
   }
-  qsdp_barrier_kernel<<<1, 32, 0, s>>>(pf, c->rank, c->world, c->epoch);
+  qsdp_barrier_kernel<<<1, 32, 0, s>>>(pf, c->rank, c->world, c->epoch());
   QSDP_CUDA(cudaGetLastError());
   return QSDP_OK;
 }
@@ -545,6 +583,36 @@ static qsdp_status check_segs(const qsdp_comm* c, const qsdp_segment* segs) {
   return QSDP_OK;
 }
 
+// Dynamic sources for one side of a collective: the quantize launch runs
+// before the barrier advances the epoch (adj 1), the dequant launch after (adj 0).
+static DynSrc comm_dyn(const qsdp_comm* c, int adj) {
+  DynSrc d;
+  d.step_ptr = c->step_src;
+  if (c->world > 1) {
+    d.parity_ptr = c->epoch();
+    d.parity_stride = c->parity_stride();
+    d.parity_adj = adj;
+  }
+  return d;
+}
+
+static QJobSpec comm_qjob(const void* x, const qsdp_segment& seg, uint8_t* slot, size_t slot_codes,
+                          const qsdp_key& key, uint64_t worker) {
+  QJobSpec q;
+  q.x = x;
+  q.length = seg.length;
+  q.global_start = seg.global_start;
+  q.codes = slot;
+  q.meta = reinterpret_cast<float*>(slot + slot_codes);
+  q.seed = key_prefix(key, worker);
+  q.key[0] = key.root_seed;
+  q.key[1] = key.step;
+  q.key[2] = key.layer;
+  q.key[3] = key.phase;
+  q.key[4] = worker;
+  return q;
+}
+
 qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, const qsdp_segment* segs,
                             const qsdp_key* key, void* full_out, int32_t out_dtype, void* stream) {
   if (c == nullptr || key == nullptr) return fail(QSDP_EINVAL, "null argument");
@@ -552,34 +620,28 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
   if (st != QSDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const qsdp_qcfg* cfg = &c->w;
-  c->epoch += 1;
-  const int par = (int)(c->epoch & 1);
   // 1. quantize this rank's shard into its local slot (key worker 0, sharded.py:341)
-  std::vector<QJobSpec> q(1);
-  q[0].x = shard;
-  q[0].length = segs[c->rank].length;
-  q[0].global_start = segs[c->rank].global_start;
-  q[0].codes = c->slot(c->base, par, 0);
-  q[0].meta = reinterpret_cast<float*>(c->slot(c->base, par, 0) + c->slot_codes);
-  q[0].seed = make_prefix(*key, 0);
-  st = run_quantize(q, in_dtype, cfg, nullptr, s);
+  std::vector<QJobSpec> q(1, comm_qjob(shard, segs[c->rank], c->slot(c->base, 0), c->slot_codes, *key, 0));
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
   if (st != QSDP_OK) return st;
   // 2. publish + wait for every peer's slot of this call
-  st = comm_barrier(c, s);
-  if (st != QSDP_OK) return st;
+  if (c->world > 1) {
+    st = comm_barrier(c, s);
+    if (st != QSDP_OK) return st;
+  }
   // 3. pull-dequantize all P shards over NVLink into the gathered buffer
   std::vector<DJobSpec> d(c->world);
   const size_t osz = dtype_size(out_dtype);
   for (int p = 0; p < c->world; ++p) {
     memset(&d[p], 0, sizeof(DJobSpec));
-    uint8_t* sl = c->slot(c->peer[p], par, 0);
+    uint8_t* sl = c->slot(c->peer[p], 0);
     d[p].codes[0] = sl;
     d[p].meta[0] = reinterpret_cast<const float*>(sl + c->slot_codes);
     d[p].nsrc = 1;
     d[p].length = segs[p].length;
     d[p].out = static_cast<uint8_t*>(full_out) + (size_t)(segs[p].global_start - segs[0].global_start) * osz;
   }
-  return run_dequant(d, cfg, 0, 1, out_dtype, s);
+  return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0));
 }
 
 qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_dtype, const qsdp_segment* segs,
@@ -589,36 +651,31 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
   if (st != QSDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const qsdp_qcfg* cfg = &c->g;
-  c->epoch += 1;
-  const int par = (int)(c->epoch & 1);
   const size_t isz = dtype_size(in_dtype);
   // 1. quantize every destination segment of this rank's gradient (worker = rank)
-  const SeedPrefix pre = make_prefix(*key, (uint64_t)c->rank);
-  std::vector<QJobSpec> q(c->world);
+  std::vector<QJobSpec> q;
   for (int p = 0; p < c->world; ++p) {
-    q[p].x = static_cast<const uint8_t*>(full_grad) + (size_t)(segs[p].global_start - segs[0].global_start) * isz;
-    q[p].length = segs[p].length;
-    q[p].global_start = segs[p].global_start;
-    q[p].codes = c->slot(c->base, par, p);
-    q[p].meta = reinterpret_cast<float*>(c->slot(c->base, par, p) + c->slot_codes);
-    q[p].seed = pre;
+    const void* x = static_cast<const uint8_t*>(full_grad) + (size_t)(segs[p].global_start - segs[0].global_start) * isz;
+    q.push_back(comm_qjob(x, segs[p], c->slot(c->base, p), c->slot_codes, *key, (uint64_t)c->rank));
   }
-  st = run_quantize(q, in_dtype, cfg, nullptr, s);
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
   if (st != QSDP_OK) return st;
-  st = comm_barrier(c, s);
-  if (st != QSDP_OK) return st;
+  if (c->world > 1) {
+    st = comm_barrier(c, s);
+    if (st != QSDP_OK) return st;
+  }
   // 3. owner pulls its segment from sources 0..P-1 (in order) and accumulates
   std::vector<DJobSpec> d(1);
   memset(&d[0], 0, sizeof(DJobSpec));
   for (int p = 0; p < c->world; ++p) {
-    uint8_t* sl = c->slot(c->peer[p], par, c->rank);
+    uint8_t* sl = c->slot(c->peer[p], c->rank);
     d[0].codes[p] = sl;
     d[0].meta[p] = reinterpret_cast<const float*>(sl + c->slot_codes);
   }
   d[0].nsrc = c->world;
   d[0].length = segs[c->rank].length;
   d[0].out = shard_out;
-  return run_dequant(d, cfg, 1, c->world, out_dtype, s);
+  return run_dequant(d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 0));
 }
 
 }  // extern "C"

@@ -116,6 +116,33 @@ __host__ __device__ __forceinline__ void seed_bucket(const SeedPrefix& pre, uint
   state = mad128(add128(inc, init), pcg_mult(), inc);
 }
 
+// SeedSequence prefix: absorb root, step, layer, phase, worker (each coerced to
+// LE uint32 words, 0 -> [0]) -- numpy mix_entropy with pool size 4.  The
+// bucket's `start` is absorbed last by seed_bucket.
+__host__ __device__ __forceinline__ SeedPrefix make_prefix(uint64_t root, uint64_t step, uint64_t layer,
+                                                           uint64_t phase, uint64_t worker) {
+  uint32_t words[10];
+  int n = 0;
+  const uint64_t f[5] = {root, step, layer, phase, worker};
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    words[n++] = (uint32_t)f[i];
+    if (f[i] >> 32) words[n++] = (uint32_t)(f[i] >> 32);
+  }
+  SeedPrefix p{};
+  uint32_t hc = SS_INIT_A;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) p.pool[i] = ss_hashmix(words[i], hc);
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+      if (s != d) p.pool[d] = ss_mix(p.pool[d], ss_hashmix(p.pool[s], hc));
+  for (int s = 4; s < n; ++s) ss_absorb(p.pool, hc, words[s]);
+  p.hash_const = hc;
+  return p;
+}
+
 // One PCG64 step (state <- state*M + inc) and XSL-RR output of the new state.
 __host__ __device__ __forceinline__ uint64_t pcg_output(U128 s) {
   const uint64_t x = s.hi ^ s.lo;
@@ -156,12 +183,13 @@ constexpr int kMaxJobs = 64;
 
 struct QJob {
   const void* x;          // segment input (element 0 of the segment)
-  uint8_t* codes;         // packed-code output
+  uint8_t* codes;         // packed-code output (parity-0 slot when the table has a parity source)
   float* meta;            // per-bucket {shift, lo, hi}
   int64_t length;         // elements in the segment
   int64_t global_start;   // key `start` of bucket 0 (sharded.py:243-248)
   int64_t bucket_base;    // prefix: global bucket index of this job's bucket 0
-  SeedPrefix seed;        // root, step, layer, phase, worker already absorbed
+  SeedPrefix seed;        // root, step, layer, phase, worker already absorbed (static step)
+  uint64_t key[5];        // raw (root, step, layer, phase, worker) for a device step source
 };
 
 struct QJobTable {
@@ -172,6 +200,14 @@ struct QJobTable {
   int32_t inner;
   int64_t total_buckets;
   unsigned long long* bad_index;  // atomicMin target: (job << 40) | element, or nullptr
+  // CUDA-graph support: if step_ptr is set, the key's step is key[1] + *step_ptr
+  // (read on the device at run time); if parity_ptr is set, outputs move by
+  // ((*parity_ptr + parity_adj) & 1) * parity_stride bytes (double-buffered slots).
+  const unsigned long long* step_ptr;
+  const unsigned long long* parity_ptr;
+  int64_t parity_stride;
+  int32_t parity_adj;
+  int32_t _pad3;
 };
 
 struct DJob {
@@ -194,7 +230,9 @@ struct DJobTable {
   int32_t accumulate;  // 0: out = dequant(src0)  1: out = (0.0 + sum_p dequant(src_p)) / divisor
   int32_t divisor;     // K4 divides the fp64 sum by this (the reference's `acc / P`)
   int32_t codes_vec;   // 1: code groups may be read with aligned 2/4/8-byte loads
-  int32_t _pad2;
+  int32_t parity_adj;
+  const unsigned long long* parity_ptr;  // sources move by ((*p + adj) & 1) * parity_stride bytes
+  int64_t parity_stride;
 };
 
 __host__ __device__ __forceinline__ int64_t payload_bytes(int64_t len, int bits) { return (len * bits + 7) / 8; }
@@ -204,6 +242,30 @@ __device__ __forceinline__ int find_job_q(const QJobTable& t, int64_t b) {
   while (j + 1 < t.njobs && t.jobs[j + 1].bucket_base <= b) ++j;
   return j;
 }
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long ld_dev_u64(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ int64_t q_parity_off(const QJobTable& t) {
+  return t.parity_ptr ? (int64_t)((ld_dev_u64(t.parity_ptr) + (unsigned long long)t.parity_adj) & 1ull) * t.parity_stride
+                      : 0;
+}
+__device__ __forceinline__ int64_t d_parity_off(const DJobTable& t) {
+  return t.parity_ptr ? (int64_t)((ld_dev_u64(t.parity_ptr) + (unsigned long long)t.parity_adj) & 1ull) * t.parity_stride
+                      : 0;
+}
+__device__ __forceinline__ SeedPrefix q_seed(const QJobTable& t, const QJob& J) {
+  if (t.step_ptr == nullptr) return J.seed;
+  return make_prefix(J.key[0], J.key[1] + ld_dev_u64(t.step_ptr), J.key[2], J.key[3], J.key[4]);
+}
+__device__ __forceinline__ float* meta_at(float* m, int64_t byte_off) {
+  return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(m) + byte_off);
+}
+__device__ __forceinline__ const float* meta_at(const float* m, int64_t byte_off) {
+  return reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(m) + byte_off);
+}
+#endif
+
 __device__ __forceinline__ int find_job_d(const DJobTable& t, int64_t b) {
   int j = 0;
   while (j + 1 < t.njobs && t.jobs[j + 1].bucket_base <= b) ++j;

@@ -359,6 +359,7 @@ __device__ __forceinline__ BucketRef resolve_q(const QJobTable& tab, int64_t b, 
 // ---------------------------------------------------------------------------
 template <typename T, int INNER, int BITS, int TL, int NST>
 __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant__ QJobTable tab, int vec) {
+  const int64_t poff = q_parity_off(tab);
   constexpr int TEAMS = 32 / TL;
   extern __shared__ __align__(128) uint8_t smem[];
   const int S = tab.bucket;
@@ -467,8 +468,8 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
     // ---- pass 2: codes ----------------------------------------------------------
     Coder<T, INNER> cd;
     float shift_f = 0.0f;
-    if (active && !degenerate) cd.setup(lof, hif, BITS, J.seed, (uint64_t)(J.global_start + br.off), lt, TL, shift_f);
-    uint8_t* cbase = J.codes + br.lb * pbs;
+    if (active && !degenerate) cd.setup(lof, hif, BITS, q_seed(tab, J), (uint64_t)(J.global_start + br.off), lt, TL, shift_f);
+    uint8_t* cbase = J.codes + poff + br.lb * pbs;
     const int64_t pb = payload_bytes(n, BITS);
     if (active && !degenerate && in_smem) {
       for (int g = 0; g < gl; ++g) {
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
       }
     }
     if (active && lt == 0) {
-      float* m = J.meta + 3 * br.lb;
+      float* m = meta_at(J.meta, poff) + 3 * br.lb;
       m[0] = degenerate ? 0.0f : shift_f;
       m[1] = lof;
       m[2] = hif;
@@ -566,7 +567,7 @@ __device__ __forceinline__ SeedOut seed_for(const QJobTable& tab, int64_t b, int
   if (b < tab.total_buckets) {
     const BucketRef br = resolve_q(tab, b, S);
     const QJob& J = tab.jobs[br.j];
-    seed_bucket(J.seed, (uint64_t)(J.global_start + br.off), o.s0, o.inc);
+    seed_bucket(q_seed(tab, J), (uint64_t)(J.global_start + br.off), o.s0, o.inc);
     if (INNER == 0) {
       const U128 s1 = mad128(o.s0, pcg_mult(), o.inc);
       const double d = u64_to_unit_double(pcg_output(s1));
@@ -605,6 +606,7 @@ struct JobCursor {
 
 template <typename T, int INNER, int BITS, int NST>
 __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_constant__ QJobTable tab) {
+  const int64_t poff = q_parity_off(tab);
   extern __shared__ __align__(128) uint8_t smem[];
   using Tr = InTraits<T>;
   using K = typename Tr::Key;
@@ -717,7 +719,7 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
     const double r = __shfl_sync(0xffffffffu, seeds.r, src_lane);
     const U128 s0 = INNER == 1 ? shfl_u128(seeds.s0, src_lane) : U128{0, 0};
     const U128 inc = INNER == 1 ? shfl_u128(seeds.inc, src_lane) : U128{0, 0};
-    uint8_t* cbase = J.codes + br.lb * pbs;
+    uint8_t* cbase = J.codes + poff + br.lb * pbs;
     const double lo = (double)lof;
     const double span = __dsub_rn((double)hif, lo);
     float shift_f = 0.0f;
@@ -787,11 +789,11 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
         }
       }
     } else if (n > 0) {
-      shift_f = quantize_bucket_general<T, INNER, BITS>(J.seed, (uint64_t)(J.global_start + br.off), in_smem ? sb : gx,
+      shift_f = quantize_bucket_general<T, INNER, BITS>(q_seed(tab, J), (uint64_t)(J.global_start + br.off), in_smem ? sb : gx,
                                                         n, gl, cbase, lof, hif, degenerate, lane);
     }
     if (lane == 0) {
-      float* m = J.meta + 3 * br.lb;
+      float* m = meta_at(J.meta, poff) + 3 * br.lb;
       m[0] = degenerate ? 0.0f : shift_f;
       m[1] = lof;
       m[2] = hif;
@@ -831,6 +833,7 @@ __device__ __forceinline__ void store_pair(uint8_t* cbase, int gi, uint64_t w, u
 
 template <typename T, int INNER, int TL, int G, bool HOLD, bool VEC>
 __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ QJobTable tab) {
+  const int64_t poff = q_parity_off(tab);
   constexpr int TEAMS = 32 / TL;
   const int lane = threadIdx.x & 31;
   const int lt = lane % TL;
@@ -898,8 +901,8 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
 
     Coder<T, INNER> cd;
     float shift_f = 0.0f;
-    if (active && !degenerate) cd.setup(lof, hif, bits, J.seed, (uint64_t)(J.global_start + br.off), lt, TL, shift_f);
-    uint8_t* cbase = J.codes + br.lb * pbs;
+    if (active && !degenerate) cd.setup(lof, hif, bits, q_seed(tab, J), (uint64_t)(J.global_start + br.off), lt, TL, shift_f);
+    uint8_t* cbase = J.codes + poff + br.lb * pbs;
     const int64_t pb = payload_bytes(n, bits);
     auto emit = [&](const T t[4], int g) {
       const int gi = g * TL + lt;
@@ -933,7 +936,7 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
       }
     }
     if (active && lt == 0) {
-      float* m = J.meta + 3 * br.lb;
+      float* m = meta_at(J.meta, poff) + 3 * br.lb;
       m[0] = degenerate ? 0.0f : shift_f;
       m[1] = lof;
       m[2] = hif;
@@ -947,6 +950,7 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
 // ---------------------------------------------------------------------------
 template <typename T, int INNER>
 __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_constant__ QJobTable tab) {
+  const int64_t poff = q_parity_off(tab);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int S = tab.bucket, bits = tab.bits;
@@ -978,7 +982,7 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
     double r = 0.0;
     float shift_f = 0.0f;
     if (!degenerate) {
-      seed_bucket(J.seed, (uint64_t)(J.global_start + br.off), st, inc);
+      seed_bucket(q_seed(tab, J), (uint64_t)(J.global_start + br.off), st, inc);
       if (INNER == 0) {
         st = mad128(st, pcg_mult(), inc);
         const double d = u64_to_unit_double(pcg_output(st));
@@ -1003,13 +1007,13 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
       acc |= (uint64_t)code << nacc;
       nacc += bits;
       while (nacc >= 8) {
-        J.codes[o++] = (uint8_t)acc;
+        J.codes[poff + o++] = (uint8_t)acc;
         acc >>= 8;
         nacc -= 8;
       }
     }
-    if (nacc > 0) J.codes[o] = (uint8_t)acc;
-    float* m = J.meta + 3 * br.lb;
+    if (nacc > 0) J.codes[poff + o] = (uint8_t)acc;
+    float* m = meta_at(J.meta, poff) + 3 * br.lb;
     m[0] = degenerate ? 0.0f : shift_f;
     m[1] = lof;
     m[2] = hif;
@@ -1088,6 +1092,7 @@ __device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, c
 // BITS > 0: direct width with aligned group loads on full buckets; BITS == 0: any width.
 template <int BITS, int TL, int OUT, bool VEC, bool ACC>
 __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJobTable tab) {
+  const int64_t poff = d_parity_off(tab);
   constexpr int TEAMS = 32 / TL;
   constexpr int U = 8;  // groups whose code words are loaded before use
   __shared__ double sm_meta[ACC ? 8 : 1][ACC ? TEAMS : 1][8][3];
@@ -1118,12 +1123,12 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
     if constexpr (!ACC) {
       double lo = 0.0, shift = 0.0, pitch = 0.0;
       if (active) {
-        const float* m = J.meta[0] + 3 * lb;
+        const float* m = meta_at(J.meta[0], poff) + 3 * lb;
         shift = (double)m[0];
         lo = (double)m[1];
         pitch = __ddiv_rn(__dsub_rn((double)m[2], lo), top);  // QuantizedBlock.pitch
       }
-      const uint8_t* __restrict__ cp = J.codes[0] + lb * pbs;
+      const uint8_t* __restrict__ cp = J.codes[0] + poff + lb * pbs;
       if (cvec && n == S) {
         for (int g0 = 0; g0 < gl; g0 += U) {
           uint64_t w[U];
@@ -1165,7 +1170,7 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
       const int nsrc = J.nsrc;
       double(*row)[3] = sm_meta[wib][team];
       if (active && lt < nsrc) {
-        const float* m = J.meta[lt] + 3 * lb;
+        const float* m = meta_at(J.meta[lt], poff) + 3 * lb;
         const double lo = (double)m[1];
         row[lt][0] = lo;
         row[lt][1] = __ddiv_rn(__dsub_rn((double)m[2], lo), top);
@@ -1181,7 +1186,7 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
           if (p < nsrc) {
-            const uint8_t* __restrict__ cp = J.codes[p] + lb * pbs;
+            const uint8_t* __restrict__ cp = J.codes[p] + poff + lb * pbs;
             w[p] = (cvec && full) ? load_group_direct<BITS>(cp, gi) : load_group_bits_any(cp, gi, bits, pb);
           }
         }
@@ -1230,9 +1235,16 @@ inline int grid_for(int64_t total_buckets, int teams_per_warp, int sms, int warp
 // second wave would only add a tail.
 template <typename F>
 inline int persistent_grid(F kern, int threads, size_t smem, int64_t total_buckets, int teams_per_warp, int sms) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
+  // one cached occupancy answer per (kernel instantiation, smem size)
+  static thread_local size_t cached_smem = (size_t)-1;
+  static thread_local int cached_threads = 0, per_sm = 1;
+  if (cached_smem != smem || cached_threads != threads) {
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, threads, smem) != cudaSuccess || v < 1) v = 1;
+    per_sm = v;
+    cached_smem = smem;
+    cached_threads = threads;
+  }
   return grid_for(total_buckets, teams_per_warp, sms, threads / 32, per_sm);
 }
 
@@ -1245,8 +1257,12 @@ cudaError_t launch_q_tma32(const QJobTable& tab, int sms, cudaStream_t s) {
   while (wpc > 2 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
   const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t);
   auto kern = quantize_tma32_kernel<T, INNER, BITS, NST>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static thread_local size_t smem_set = 0;  // per instantiation: set once, not during graph capture
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
   const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, 1, sms);
   kern<<<grid, wpc * 32, smem, s>>>(tab);
   return cudaGetLastError();
@@ -1265,8 +1281,12 @@ cudaError_t launch_q_tma(const QJobTable& tab, bool vec, int sms, cudaStream_t s
     while (wpc > 1 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t);
     auto kern = quantize_tma_kernel<T, INNER, BITS, TL, NST>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    static thread_local size_t smem_set = 0;
+    if (smem > smem_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      smem_set = smem;
+    }
     const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, TEAMS, sms);
     kern<<<grid, wpc * 32, smem, s>>>(tab, vec ? 1 : 0);
     return cudaGetLastError();

@@ -31,7 +31,7 @@ __all__ = [
     "QuantSpec", "SegmentKey", "BucketSpec", "QuantizedBlock", "KeyedBucketRNG", "bucket_rng",
     "num_buckets", "codes_bytes", "message_size_bits", "quantize_segments", "quantize_segment",
     "dequantize_segments", "dequantize_segment", "dequant_accumulate", "quantize_bucket",
-    "bucketed_quantize", "dequantize", "INNER_MODES",
+    "bucketed_quantize", "dequantize", "INNER_MODES", "advance_counter",
 ]
 
 AFFINE_MODES = ("shift", "flip", "uniform_stochastic")
@@ -113,7 +113,15 @@ def _bad_to_error(bad: int, items) -> None:
     raise ValueError(f"non-finite bucket value at index {idx}: {v!r}")
 
 
-def quantize_segments(items, spec: QuantSpec, check_finite: bool = False, out=None):
+def advance_counter(counter: torch.Tensor, delta: int = 1) -> None:
+    """``counter += delta`` on the current stream via the library (graph-capturable)."""
+    if counter.dtype != torch.int64 or not counter.is_cuda:
+        raise ValueError("counter must be a CUDA int64 tensor")
+    with torch.cuda.device(counter.device):
+        _lib.check(_lib.lib().qsdp_counter_add(counter.data_ptr(), int(delta), _stream(counter.device)))
+
+
+def quantize_segments(items, spec: QuantSpec, check_finite: bool = False, out=None, step_src=None):
     """Quantize several segments in one launch.
 
     ``items``: list of ``(x, global_start, SegmentKey)`` with ``x`` a contiguous
@@ -122,6 +130,8 @@ def quantize_segments(items, spec: QuantSpec, check_finite: bool = False, out=No
     ``(codes uint8[codes_bytes], meta float32[nb, 3])``.  With
     ``check_finite`` the call synchronises and raises ``ValueError`` naming the
     first non-finite element, like ``_check_finite`` (quantize.py:41-44).
+    ``step_src`` (CUDA int64 scalar tensor): keys use ``step + step_src`` read on
+    the device, so a captured CUDA graph replays with fresh noise per step.
     """
     if not items:
         return []
@@ -154,9 +164,10 @@ def quantize_segments(items, spec: QuantSpec, check_finite: bool = False, out=No
         bad = torch.full((1,), -1, dtype=torch.int64, device=dev)  # all ones == UINT64_MAX
     cfg = spec.cfg()
     with torch.cuda.device(dev):
-        _lib.check(_lib.lib().qsdp_quantize_batch(
+        _lib.check(_lib.lib().qsdp_quantize_batch_dstep(
             arr, len(items), _DTYPE_CODE[dt], ctypes.byref(cfg),
-            bad.data_ptr() if bad is not None else None, _stream(dev)))
+            bad.data_ptr() if bad is not None else None,
+            step_src.data_ptr() if step_src is not None else None, _stream(dev)))
     if bad is not None:
         _bad_to_error(int(bad.item()) & ((1 << 64) - 1), items)
     return outs

@@ -55,6 +55,44 @@ def main():
             if not (ok_ag and ok_rs):
                 failures += 1
                 print(f"rank {rank} size {size} step {step}: ag {ok_ag} rs {ok_rs}", flush=True)
+        # graph capture of one AG + RS with the step read on the device (epoch on device too)
+        from paper_2302_02390_b200.quantize import advance_counter
+        ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+        comm.set_step_source(ctr)
+        s, n = segs[rank]
+        shard = torch.from_numpy(full[s:s + n]).to(dev)
+        out = torch.empty(size, dtype=torch.float32, device=dev)
+        g = torch.from_numpy(grads[rank]).to(dev)
+        sh = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+
+        def step():
+            comm.all_gather(shard, segs, SegmentKey(0, 100, 4, 0, 0), out)
+            comm.reduce_scatter(g, segs, SegmentKey(0, 100, 4, 2, rank), sh)
+            advance_counter(ctr)
+        step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for rep in range(3):
+            stepno = int(ctr.item())
+            graph.replay()
+            torch.cuda.synchronize()
+            exp = np.zeros(size)
+            for q, (sq, nq) in enumerate(segs):
+                if nq:
+                    c, m, _ = O.quantize_segment(full[sq:sq + nq], sq, bucket, wb, 0, (0, 100 + stepno, 4, 0, 0), 8)
+                    exp[sq:sq + nq] = O.dequantize_segment(c, m, nq, bucket, wb, 8)
+            acc = np.zeros(n)
+            for p in range(world):
+                if n:
+                    c, m, _ = O.quantize_segment(grads[p][s:s + n], s, bucket, gb, 1, (0, 100 + stepno, 4, 2, p), 8)
+                    acc = acc + O.dequantize_segment(c, m, n, bucket, gb, 8)
+            ok = np.array_equal(out.cpu().numpy(), exp.astype(np.float32)) and \
+                np.array_equal(sh[:n].cpu().numpy(), (acc / world).astype(np.float32))
+            if not ok:
+                failures += 1
+                print(f"rank {rank} size {size} graph replay {rep}: mismatch", flush=True)
         comm.close()
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)

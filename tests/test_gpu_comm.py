@@ -36,6 +36,40 @@ def test_single_rank_comm_vs_oracle(oracle):
     comm.close()
 
 
+def test_graph_replay_with_device_step(oracle):
+    """A captured AG+RS replays with the step read on the device (fresh noise per replay)."""
+    from paper_2302_02390_b200.quantize import advance_counter
+    dev = torch.device("cuda", 0)
+    size = 70000
+    comm = QSDPComm(size, QuantSpec(8, 1024, "shift"), QuantSpec(4, 1024, "uniform_stochastic"), device=dev)
+    ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+    comm.set_step_source(ctr)
+    x = (np.random.default_rng(3).standard_normal(size) * 0.02).astype(np.float32)
+    xt = torch.from_numpy(x).to(dev)
+    out = torch.empty(size, device=dev)
+    sh = torch.empty(size, device=dev)
+
+    def step():
+        comm.all_gather(xt, [(0, size)], SegmentKey(0, 10, 1, 0, 0), out)
+        comm.reduce_scatter(xt, [(0, size)], SegmentKey(0, 10, 1, 2, 0), sh)
+        advance_counter(ctr)
+
+    step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for rep in range(2):
+        stepno = int(ctr.item())
+        g.replay()
+        torch.cuda.synchronize()
+        c, m, _ = oracle.quantize_segment(x, 0, 1024, 8, 0, (0, 10 + stepno, 1, 0, 0), 8)
+        assert np.array_equal(out.cpu().numpy(), oracle.dequantize_segment(c, m, size, 1024, 8, 8).astype(np.float32))
+        c, m, _ = oracle.quantize_segment(x, 0, 1024, 4, 1, (0, 10 + stepno, 1, 2, 0), 8)
+        assert np.array_equal(sh.cpu().numpy(), oracle.dequantize_segment(c, m, size, 1024, 4, 8).astype(np.float32))
+    comm.close()
+
+
 def test_plan_segments():
     assert plan_segments(10, 4) == [(0, 2), (2, 2), (4, 2), (6, 4)]
     assert plan_segments(10, 4, pad_to=4) == [(0, 4), (4, 4), (8, 2), (10, 0)]
