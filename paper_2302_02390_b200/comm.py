@@ -22,7 +22,7 @@ import torch.distributed as dist
 from . import _lib
 from .quantize import QuantSpec, SegmentKey, _DTYPE_CODE
 
-__all__ = ["QSDPComm", "plan_segments"]
+__all__ = ["QSDPComm", "plan_segments", "all_gather_plan", "reduce_scatter_plan", "sent_bits"]
 
 
 def plan_segments(size: int, world: int, pad_to: int = 1):
@@ -44,6 +44,47 @@ def plan_segments(size: int, world: int, pad_to: int = 1):
         s = min(p * per, size)
         segs.append((s, max(0, min(per, size - s))))
     return segs
+
+
+def all_gather_plan(rank: int, world: int, segs, key: SegmentKey):
+    """What rank ``rank`` does in one quantized all-gather (sharded.py:323-373).
+
+    Returns ``(quantize, pull)``: ``quantize`` = [(global_start, length, key)] for
+    its own shard (worker 0, the shard's global start); ``pull`` = [(src_rank,
+    out_offset, length)] -- every rank's slot, dequantized into the gathered
+    tensor at the segment's offset.  This is the schedule the C ABI executes.
+    """
+    k = SegmentKey(key.root_seed, key.step, key.layer, key.phase, 0)
+    s, n = segs[rank]
+    quantize = [(s, n, k)] if n > 0 else []
+    base = segs[0][0]
+    pull = [(p, segs[p][0] - base, segs[p][1]) for p in range(world) if segs[p][1] > 0]
+    return quantize, pull
+
+
+def reduce_scatter_plan(rank: int, world: int, segs, key: SegmentKey):
+    """What rank ``rank`` does in one quantized reduce-scatter (sharded.py:375-433).
+
+    ``quantize`` = [(dst, global_start, length, key)] for every destination
+    segment of its gradient (worker = rank); ``pull`` = the sources 0..P-1 whose
+    slot ``rank`` are dequant-accumulated in order, then divided by ``world``.
+    """
+    k = SegmentKey(key.root_seed, key.step, key.layer, key.phase, rank)
+    quantize = [(q, segs[q][0], segs[q][1], k) for q in range(world) if segs[q][1] > 0]
+    pull = list(range(world)) if segs[rank][1] > 0 else []
+    return quantize, pull
+
+
+def sent_bits(kind: str, rank: int, world: int, segs, spec: QuantSpec) -> int:
+    """Wire bits this rank puts on the links for one collective -- the reference
+    ledger's records restricted to the sender (sharded.py:349-358, 403-413): an
+    all-gather message crosses to world-1 peers, a reduce-scatter segment to its
+    owner (the self-contribution is free)."""
+    from .quantize import message_size_bits
+    if kind == "allgather":
+        n = segs[rank][1]
+        return message_size_bits(n, spec) * (world - 1) if n > 0 else 0
+    return sum(message_size_bits(segs[q][1], spec) for q in range(world) if q != rank and segs[q][1] > 0)
 
 
 class QSDPComm:

@@ -206,7 +206,7 @@ class QSDPHooks:
         dev = self._qsdp_dev()
         full = torch.from_numpy(np.ascontiguousarray(np.concatenate(shards), dtype=np.float64)).to(dev)
         if quantized:
-            spec = quant.weight_spec()
+            spec = QuantSpec(quant.weight_bits, quant.bucket_size, "shift")
             out = gather_segments(full, bounds, spec,
                                   SegmentKey(self.cfg.root_seed, step, layer_idx, phase, 0))
             for s, e in bounds:
@@ -234,7 +234,7 @@ class QSDPHooks:
         g = torch.from_numpy(np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.float64).ravel()
                                                             for x in per_worker_grads]))).to(dev)
         if quantized:
-            spec = quant.gradient_spec()
+            spec = QuantSpec(quant.gradient_bits, quant.bucket_size, "uniform_stochastic")
             outs = reduce_scatter_segments(g, bounds, spec, self.cfg.root_seed, step, layer_idx)
             for q, (s, e) in enumerate(bounds):
                 if e == s:
