@@ -253,8 +253,8 @@ struct Coder {
       const Fixed32 q = fixed32(__dmul_rn(u, top));
       const uint32_t dh = pcg_output_hi32(st);
       if (at_hi || at_lo) return (uint32_t)q.ip;  // s exact integer, frac 0: d < 0 is false
-      // uncertain iff fq in {dh, dh+1} or the floor itself is uncertain (fq == 0)
-      if (q.frac == 0u || q.frac - dh <= 1u) return exact_stoch_code(a, span, top, st);
+      // uncertain iff (fq - dh) mod 2^32 <= 1 (covers fq == 0 too)
+      if (q.frac - dh <= 1u) return exact_stoch_code(a, span, top, st);
       const int c = q.ip + (q.frac > dh ? 1 : 0);
       return (uint32_t)min(c, (int)top);
     }
@@ -553,6 +553,37 @@ static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix
 
 constexpr double kMagic = 1572864.0;  // 1.5 * 2^20
 
+// Store the 8 packed codes of octet o (8*BITS bits = BITS bytes, aligned).
+template <int BITS>
+__device__ __forceinline__ void store_octet(uint8_t* base, int o, uint64_t w) {
+  if (BITS == 8) reinterpret_cast<unsigned long long*>(base)[o] = w;
+  else if (BITS == 4) reinterpret_cast<uint32_t*>(base)[o] = (uint32_t)w;
+  else if (BITS == 2) reinterpret_cast<uint16_t*>(base)[o] = (uint16_t)w;
+  else base[o] = (uint8_t)w;  // BITS == 16 never takes the octet path (64-bit word holds 4 codes)
+}
+
+// Rare path of the octet loop: recompute the 8 codes, certifying each element
+// again and falling back to the exact chain where the bound is not met.
+template <typename T, int BITS>
+static __device__ __noinline__ uint64_t stoch_octet_exact(const T* v, U128 st, U128 inc, double lo, double span,
+                                                          double K1, double top) {
+  using Tr = InTraits<T>;
+  uint64_t w = 0;
+  for (int i = 0; i < 8; ++i) {
+    double a = __dsub_rn(Tr::to_d(v[i]), lo);
+    if constexpr (sizeof(T) == 8) a = fmin(fmax(a, 0.0), span);
+    const double y = __fma_rn(a, K1, kMagic);
+    const uint32_t fq = (uint32_t)__double2loint(y);
+    const uint32_t ip = (uint32_t)__double2hiint(y) & 0x7FFFFu;
+    const uint32_t dh = pcg_output_hi32(st);
+    uint32_t c = ip + (fq > dh ? 1u : 0u);
+    if ((fq - dh) <= 1u) c = exact_stoch_code(__dsub_rn(Tr::to_d(v[i]), lo), span, top, st);
+    w |= (uint64_t)c << (i * BITS);
+    st = mad128(st, pcg_mult(), inc);
+  }
+  return w;
+}
+
 struct SeedOut {
   U128 s0, inc;
   double r;
@@ -626,12 +657,6 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
   const double pitch = __ddiv_rn(1.0, top);
 
   // per-lane jump constants: lane starts at element 4*lane, groups are 128 apart
-  U128 A0{1, 0}, G0{0, 0}, JA{1, 0}, JG{0, 0};
-  if (INNER == 1) {
-    const JumpEntry e0 = g_jump[4 * lane + 1];
-    const JumpEntry ej = g_jump[4 * 32 - 3];
-    A0 = e0.a; G0 = e0.g; JA = ej.a; JG = ej.g;
-  }
 
   if (lane == 0) {
 #pragma unroll
@@ -758,9 +783,48 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
             store_direct<BITS>(cbase, gi, w, 0, true);
           }
         }
+      } else if (BITS != 16 && (S & 255) == 0) {
+        if constexpr (BITS != 16) {
+        // octets: lane owns 8 consecutive elements 8*o (o = lane, lane+32, ...), so the
+        // stream jumps once per 8 draws (by 256-7) instead of once per 4.
+        // jump constants from the (L1-resident) table, per bucket: keeps registers for the loop
+        const JumpEntry o0 = g_jump[8 * lane + 1];
+        U128 st = add128(mul128(o0.a, s0), mul128(o0.g, inc));  // state_{8*lane+1}
+        const JumpEntry oj = g_jump[8 * 32 - 7];
+        const U128 OJa = oj.a;
+        const U128 jc = mul128(oj.g, inc);
+        const int ol = S / 256;
+        for (int g = 0; g < ol; ++g) {
+          const int o = g * 32 + lane;
+          T v[8];
+          lds_group(sb, 8 * o, v);
+          lds_group(sb, 8 * o + 4, v + 4);
+          const U128 st0 = st;
+          uint64_t w = 0;
+          bool unc = false;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            double a = __dsub_rn(Tr::to_d(v[i]), lo);
+            if constexpr (sizeof(T) == 8) a = fmin(fmax(a, 0.0), span);
+            const double y = __fma_rn(a, K1, kMagic);
+            const uint32_t fq = (uint32_t)__double2loint(y);
+            const uint32_t ip = (uint32_t)__double2hiint(y) & 0x7FFFFu;  // s >= 0: drop the 2^19 offset bit
+            const uint32_t dh = pcg_output_hi32(st);
+            unc |= (fq - dh) <= 1u;  // the only uncertain case
+            w |= (uint64_t)(ip + (fq > dh ? 1u : 0u)) << (i * BITS);
+            if (i < 7) st = mad128(st, pcg_mult(), inc);
+          }
+          if (unc) w = stoch_octet_exact<T, BITS>(sb + 8 * o, st0, inc, lo, span, K1, top);
+          store_octet<BITS>(cbase, o, w);
+          st = add128(mul128(OJa, st), jc);
+        }
+        }
       } else {
-        U128 st = add128(mul128(A0, s0), mul128(G0, inc));  // state_{4*lane+1}
-        const U128 jc = mul128(JG, inc);
+        const JumpEntry e0 = g_jump[4 * lane + 1];
+        U128 st = add128(mul128(e0.a, s0), mul128(e0.g, inc));  // state_{4*lane+1}
+        const JumpEntry ej = g_jump[4 * 32 - 3];
+        const U128 JA = ej.a;
+        const U128 jc = mul128(ej.g, inc);
 #pragma unroll 2
         for (int g = 0; g < gl; ++g) {
           const int gi = g * 32 + lane;
@@ -778,7 +842,7 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
               const uint32_t ip = (uint32_t)__double2hiint(y) & 0x7FFFFu;  // s >= 0: drop the 2^19 offset bit
               const uint32_t dh = pcg_output_hi32(st);
               uint32_t c = ip + (fq > dh ? 1u : 0u);
-              const bool unc = (fq - dh) <= 1u || (fq == 0u && v[i] != mnv && v[i] != mxv);
+              const bool unc = (fq - dh) <= 1u;
               if (unc) c = exact_stoch_code(__dsub_rn(Tr::to_d(v[i]), lo), span, top, st);
               w |= (uint64_t)c << (i * BITS);
               if (i < 3) st = mad128(st, pcg_mult(), inc);
@@ -1177,36 +1241,45 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
         row[lt][2] = (double)m[0];
       }
       __syncwarp();
-      for (int g = 0; g < gl; ++g) {
-        const int gi = g * TL + lt;
-        const int e = 4 * gi;
-        if (e >= n) break;
-        const bool full = e + 4 <= n;
-        uint64_t w[8];
+      constexpr int UA = 4;  // groups accumulated together (their code loads are in flight together)
+      for (int g0 = 0; g0 < gl; g0 += UA) {
+        double acc[UA][4];
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          if (p < nsrc) {
-            const uint8_t* __restrict__ cp = J.codes[p] + poff + lb * pbs;
-            w[p] = (cvec && full) ? load_group_direct<BITS>(cp, gi) : load_group_bits_any(cp, gi, bits, pb);
+        for (int u = 0; u < UA; ++u)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[u][i] = 0.0;
+        for (int p = 0; p < nsrc; ++p) {
+          const uint8_t* __restrict__ cp = J.codes[p] + poff + lb * pbs;
+          uint64_t w[UA];
+#pragma unroll
+          for (int u = 0; u < UA; ++u) {
+            const int gi = (g0 + u) * TL + lt;
+            const int e = 4 * gi;
+            w[u] = 0;
+            if (g0 + u < gl && e < n)
+              w[u] = (cvec && e + 4 <= n) ? load_group_direct<BITS>(cp, gi) : load_group_bits_any(cp, gi, bits, pb);
           }
-        }
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          const double lo = row[p][0], pitch = row[p][1], shift = row[p][2];
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          if (p < nsrc) {
-            const double lo = row[p][0], pitch = row[p][1], shift = row[p][2];
+          for (int u = 0; u < UA; ++u)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const double c = code_to_double((uint32_t)((w[p] >> (i * bits)) & cmask));
-              acc[i] = __dadd_rn(acc[i], __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift));
+              const double c = code_to_double((uint32_t)((w[u] >> (i * bits)) & cmask));
+              acc[u][i] = __dadd_rn(acc[u][i], __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift));
             }
+        }
+#pragma unroll
+        for (int u = 0; u < UA; ++u) {
+          const int gi = (g0 + u) * TL + lt;
+          const int e = 4 * gi;
+          if (g0 + u < gl && e < n) {
+            if (tab.divisor != 1) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[u][i] = __ddiv_rn(acc[u][i], (double)tab.divisor);
+            }
+            store_out4<OUT, VEC>(J.out, off + e, n - e, acc[u]);
           }
         }
-        if (tab.divisor != 1) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) acc[i] = __ddiv_rn(acc[i], (double)tab.divisor);
-        }
-        store_out4<OUT, VEC>(J.out, off + e, n - e, acc);
       }
       __syncwarp();
     }
