@@ -648,6 +648,9 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
   const int wpc = blockDim.x >> 5;
   T* wbuf = reinterpret_cast<T*>(smem) + (int64_t)wib * NST * S;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)wpc * NST * S * sizeof(T)) + wib * NST;
+  // lane-parallel seeds of the warp's next 32 buckets live in shared memory
+  SeedOut* seeds = reinterpret_cast<SeedOut*>(smem + (size_t)wpc * NST * S * sizeof(T) +
+                                              (size_t)wpc * NST * sizeof(uint64_t)) + wib * 32;
   const int64_t gw = (int64_t)blockIdx.x * wpc + wib;
   const int64_t nw = (int64_t)gridDim.x * wpc;
   const int64_t total = tab.total_buckets;
@@ -685,9 +688,12 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
   for (int64_t k = 0; k < NST; ++k)
     if (bucket_of(k) < total) issue(k);
 
-  SeedOut seeds{};
   for (int64_t k = 0; bucket_of(k) < total; ++k) {
-    if ((k & 31) == 0) seeds = seed_for<INNER>(tab, bucket_of(k + lane), S, pitch);
+    if ((k & 31) == 0) {
+      __syncwarp();
+      seeds[lane] = seed_for<INNER>(tab, bucket_of(k + lane), S, pitch);
+      __syncwarp();
+    }
     const int stage = (int)(k % NST);
     const int64_t b = bucket_of(k);
     const BucketRef br = mcur.get(tab, b, S);
@@ -740,10 +746,10 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
     }
 
     // ---- pass 2: codes --------------------------------------------------------
-    const int src_lane = (int)(k & 31);
-    const double r = __shfl_sync(0xffffffffu, seeds.r, src_lane);
-    const U128 s0 = INNER == 1 ? shfl_u128(seeds.s0, src_lane) : U128{0, 0};
-    const U128 inc = INNER == 1 ? shfl_u128(seeds.inc, src_lane) : U128{0, 0};
+    const SeedOut& sd = seeds[k & 31];  // smem broadcast
+    const double r = INNER == 0 ? sd.r : 0.0;
+    const U128 s0 = INNER == 1 ? sd.s0 : U128{0, 0};
+    const U128 inc = INNER == 1 ? sd.inc : U128{0, 0};
     uint8_t* cbase = J.codes + poff + br.lb * pbs;
     const double lo = (double)lof;
     const double span = __dsub_rn((double)hif, lo);
@@ -1328,7 +1334,8 @@ cudaError_t launch_q_tma32(const QJobTable& tab, int sms, cudaStream_t s) {
   const size_t stage = (size_t)tab.bucket * sizeof(T);
   int wpc = 8;
   while (wpc > 2 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
-  const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t);
+  const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t) +
+                      (size_t)wpc * 32 * sizeof(SeedOut);
   auto kern = quantize_tma32_kernel<T, INNER, BITS, NST>;
   static thread_local size_t smem_set = 0;  // per instantiation: set once, not during graph capture
   if (smem > smem_set) {
