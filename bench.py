@@ -238,6 +238,8 @@ def main():
     step_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
     comm = QSDPComm(max_seg, wspec, gspec, device=dev)
     comm.set_step_source(step_ctr)
+    comm_fused = os.environ.get("QSDP_FUSED", "0") == "1" and args.bucket % 8 == 0 and 128 <= args.bucket <= 2048 \
+        and args.wbits in (2, 4, 8, 16) and args.gbits in (2, 4, 8, 16)
     stream = torch.cuda.current_stream(dev)
 
     # ---- the step as a list of launches (kind, bytes, fn) ----
@@ -284,15 +286,22 @@ def main():
                 st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"])))
         return L
 
-    launches = local_launches() if world == 1 else comm_launches()
-    n_launch = (sum(1 for _ in launches) if world == 1 else sum(x[1] for x in launches)) + 1  # + counter
+    # `value` times the product path (the communicator: one fused launch per collective when
+    # possible); the per-kernel roofline graphs replay the same kernels through the batch API.
+    launches = comm_launches()
+    klaunches = local_launches() if world == 1 else []
+    per_coll = 1 if comm_fused else (3 if world > 1 else 2)
+    n_launch = len(launches) * per_coll + 1  # + step counter
 
     def run_step(sel=None):
-        for kind, _, fn in launches:
-            if sel is None or kind == sel:
-                fn()
         if sel is None:
+            for _, _, fn in launches:
+                fn()
             advance_counter(step_ctr)
+        else:
+            for kind, _, fn in klaunches:
+                if kind == sel:
+                    fn()
 
     def barrier():
         if world > 1:
@@ -347,8 +356,8 @@ def main():
     kernels, roofline = {}, None
     if world == 1:
         for k in kinds:
-            nb = sum(x[1] for x in launches if x[0] == k)
-            cnt = sum(1 for x in launches if x[0] == k)
+            nb = sum(x[1] for x in klaunches if x[0] == k)
+            cnt = sum(1 for x in klaunches if x[0] == k)
             gk = capture(lambda k=k: run_step(k))
             gk.replay()
             torch.cuda.synchronize(dev)
@@ -424,7 +433,8 @@ def main():
                                    f"AG fwd + AG bwd + RS over {len(groups)} FSDP groups ({N_total} dense params)",
                        "out_dtype": args.out_dtype, "quantizer_input": "f32", "arithmetic": "f64 (bit-exact)",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 126 MB L2",
-                       "parallelism": f"qsdp{world}", "execution": "one CUDA graph per step (device step counter)",
+                       "parallelism": f"qsdp{world}", "execution": "one CUDA graph per step (device step counter), "
+                                    + ("fused single-launch collectives" if comm_fused else "3 launches per collective"),
                        "convention": "sum over ranks of 4*N per collective / time"},
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),

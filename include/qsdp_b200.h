@@ -161,6 +161,10 @@ qsdp_status qsdp_comm_open_peers(qsdp_comm* c, const void* handles /* world*QSDP
  * With it, and the communicator's device-side epoch, a sequence of
  * qsdp_all_gather / qsdp_reduce_scatter calls can be captured in a CUDA graph. */
 qsdp_status qsdp_comm_set_step_source(qsdp_comm* c, const uint64_t* d_step);
+/* 1 (opt-in; env QSDP_FUSED=1 sets it at creation): run each collective as ONE persistent
+ * kernel -- quantize, in-kernel grid + cross-GPU barrier, pull-dequantize -- when the
+ * configuration allows (fp32 input, 2/4/8/16 bits, bucket 128..2048, aligned output). */
+qsdp_status qsdp_comm_set_fused(qsdp_comm* c, int32_t enable);
 /* Quantized all-gather (ShardedMLP._gather): this rank's shard = segs[rank];
  * every rank writes the dequantized full tensor (sum of segs lengths) to full_out.
  * key->worker is forced to 0 (sharded.py:341). */

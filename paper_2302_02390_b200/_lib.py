@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = (
     "qsdp_dequantize_batch", "qsdp_dequant_accumulate", "qsdp_dequant_accumulate_batch",
     "qsdp_wire_encode", "qsdp_comm_create", "qsdp_comm_ipc_handle", "qsdp_comm_open_peers",
     "qsdp_all_gather", "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_batch_dstep",
-    "qsdp_counter_add", "qsdp_comm_set_step_source",
+    "qsdp_counter_add", "qsdp_comm_set_step_source", "qsdp_comm_set_fused",
 )
 
 
@@ -104,6 +104,7 @@ def lib():
     L.qsdp_quantize_batch_dstep.argtypes = [ctypes.POINTER(QItem), i32, i32, cfgp, vp, vp, vp]
     L.qsdp_counter_add.argtypes = [vp, ctypes.c_uint64, vp]
     L.qsdp_comm_set_step_source.argtypes = [vp, vp]
+    L.qsdp_comm_set_fused.argtypes = [vp, i32]
     L.qsdp_dequantize.argtypes = [vp, vp, i64, cfgp, vp, i32, vp]
     L.qsdp_dequantize_batch.argtypes = [ctypes.POINTER(DItem), i32, cfgp, i32, vp]
     L.qsdp_dequant_accumulate.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i64, cfgp,
@@ -118,7 +119,7 @@ def lib():
     L.qsdp_reduce_scatter.argtypes = [vp, vp, i32, segp, keyp, vp, i32, vp]
     L.qsdp_comm_destroy.argtypes = [vp]
     for name in ("qsdp_quantize", "qsdp_quantize_batch", "qsdp_quantize_batch_dstep", "qsdp_counter_add",
-                 "qsdp_comm_set_step_source", "qsdp_dequantize", "qsdp_dequantize_batch",
+                 "qsdp_comm_set_step_source", "qsdp_comm_set_fused", "qsdp_dequantize", "qsdp_dequantize_batch",
                  "qsdp_dequant_accumulate", "qsdp_dequant_accumulate_batch", "qsdp_comm_create",
                  "qsdp_comm_ipc_handle", "qsdp_comm_open_peers", "qsdp_all_gather",
                  "qsdp_reduce_scatter", "qsdp_comm_destroy"):

@@ -126,6 +126,10 @@ class QSDPComm:
         self._step_src = counter  # keep alive
         _lib.check(_lib.lib().qsdp_comm_set_step_source(self._h, counter.data_ptr() if counter is not None else None))
 
+    def set_fused(self, enable: bool) -> None:
+        """Single-launch fused collectives (default on when the configuration allows)."""
+        _lib.check(_lib.lib().qsdp_comm_set_fused(self._h, 1 if enable else 0))
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             _lib.lib().qsdp_comm_destroy(self._h)

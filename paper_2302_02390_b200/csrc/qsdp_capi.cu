@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -32,6 +33,8 @@ cudaError_t launch_quantize_f64(const QJobTable& tab, bool vec, int sms, cudaStr
 cudaError_t launch_dequant(const DJobTable& tab, bool vec, int sms, cudaStream_t s);
 cudaError_t upload_jump_f32(const JumpEntry* host);
 cudaError_t upload_jump_f64(const JumpEntry* host);
+cudaError_t upload_jump_fused(const JumpEntry* host);
+cudaError_t launch_fused(const QJobTable& qt, const DJobTable& dt, const FuseSync& fs, int sms, cudaStream_t s);
 }  // namespace qsdp
 
 using namespace qsdp;
@@ -80,6 +83,7 @@ qsdp_status ensure_device(int& sms) {
     }
     QSDP_CUDA(upload_jump_f32(tab));
     QSDP_CUDA(upload_jump_f64(tab));
+    QSDP_CUDA(upload_jump_fused(tab));
     QSDP_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
     d.jump_ready = true;
   }
@@ -123,47 +127,52 @@ struct DynSrc {
   int32_t parity_adj = 0;
 };
 
+// Table builders shared by the launch-per-stage path and the fused collectives.
+void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, const qsdp_qcfg* cfg, uint64_t* d_bad,
+                const DynSrc& dyn, bool& vec) {
+  memset(&tab, 0, sizeof(tab));
+  tab.bits = cfg->bits;
+  tab.bucket = cfg->bucket;
+  tab.inner = cfg->inner;
+  tab.bad_index = reinterpret_cast<unsigned long long*>(d_bad);
+  tab.step_ptr = dyn.step_ptr;
+  tab.parity_ptr = dyn.parity_ptr;
+  tab.parity_stride = dyn.parity_stride;
+  tab.parity_adj = dyn.parity_adj;
+  int64_t nb = 0;
+  vec = cfg->bucket % 4 == 0;
+  int nj = 0;
+  for (; i < jobs.size() && nj < kMaxJobs; ++i) {
+    const QJobSpec& s = jobs[i];
+    if (s.length <= 0) continue;
+    QJob& J = tab.jobs[nj++];
+    J.x = s.x;
+    J.codes = s.codes;
+    J.meta = s.meta;
+    J.length = s.length;
+    J.global_start = s.global_start;
+    J.bucket_base = nb;
+    J.seed = s.seed;
+    for (int w = 0; w < 5; ++w) J.key[w] = s.key[w];
+    nb += (s.length + cfg->bucket - 1) / cfg->bucket;
+    vec = vec && aligned(s.x, 16);
+  }
+  tab.njobs = nj;
+  tab.total_buckets = nb;
+}
+
 qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const qsdp_qcfg* cfg,
                          uint64_t* d_bad, cudaStream_t stream, const DynSrc& dyn = DynSrc()) {
   if (x_dtype != QSDP_F32 && x_dtype != QSDP_F64) return fail(QSDP_EINVAL, "input dtype must be f32 or f64");
   int sms = 0;
   qsdp_status st = ensure_device(sms);
   if (st != QSDP_OK) return st;
-  const size_t esz = dtype_size(x_dtype);
   size_t i = 0;
   while (i < jobs.size()) {
     QJobTable tab;
-    memset(&tab, 0, sizeof(tab));
-    tab.bits = cfg->bits;
-    tab.bucket = cfg->bucket;
-    tab.inner = cfg->inner;
-    tab.bad_index = reinterpret_cast<unsigned long long*>(d_bad);
-    tab.step_ptr = dyn.step_ptr;
-    tab.parity_ptr = dyn.parity_ptr;
-    tab.parity_stride = dyn.parity_stride;
-    tab.parity_adj = dyn.parity_adj;
-    int64_t nb = 0;
-    bool vec = cfg->bucket % 4 == 0;
-    int nj = 0;
-    for (; i < jobs.size() && nj < kMaxJobs; ++i) {
-      const QJobSpec& s = jobs[i];
-      if (s.length <= 0) continue;
-      QJob& J = tab.jobs[nj++];
-      J.x = s.x;
-      J.codes = s.codes;
-      J.meta = s.meta;
-      J.length = s.length;
-      J.global_start = s.global_start;
-      J.bucket_base = nb;
-      J.seed = s.seed;
-      for (int w = 0; w < 5; ++w) J.key[w] = s.key[w];
-      nb += (s.length + cfg->bucket - 1) / cfg->bucket;
-      vec = vec && aligned(s.x, 16);
-      (void)esz;
-    }
-    tab.njobs = nj;
-    tab.total_buckets = nb;
-    if (nj == 0) continue;
+    bool vec = false;
+    build_qtab(tab, jobs, i, cfg, d_bad, dyn, vec);
+    if (tab.njobs == 0) continue;
     cudaError_t e = x_dtype == QSDP_F64 ? launch_quantize_f64(tab, vec, sms, stream)
                                          : launch_quantize_f32(tab, vec, sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "quantize kernel launch");
@@ -179,6 +188,42 @@ struct DJobSpec {
   void* out;
 };
 
+void build_dtab(DJobTable& tab, const std::vector<DJobSpec>& jobs, size_t& i, const qsdp_qcfg* cfg, int accumulate,
+                int divisor, int out_dtype, const DynSrc& dyn, bool& vec) {
+  memset(&tab, 0, sizeof(tab));
+  tab.bits = cfg->bits;
+  tab.bucket = cfg->bucket;
+  tab.out_dtype = out_dtype;
+  tab.accumulate = accumulate;
+  tab.divisor = divisor < 1 ? 1 : divisor;
+  tab.parity_ptr = dyn.parity_ptr;
+  tab.parity_stride = dyn.parity_stride;
+  tab.parity_adj = dyn.parity_adj;
+  vec = cfg->bucket % 4 == 0;
+  bool cvec = cfg->bucket % 8 == 0;
+  int64_t nb = 0;
+  int nj = 0;
+  for (; i < jobs.size() && nj < kMaxJobs; ++i) {
+    const DJobSpec& s = jobs[i];
+    if (s.length <= 0) continue;
+    DJob& J = tab.jobs[nj++];
+    for (int p = 0; p < s.nsrc; ++p) {
+      J.codes[p] = s.codes[p];
+      J.meta[p] = s.meta[p];
+      cvec = cvec && aligned(s.codes[p], 8);
+    }
+    J.nsrc = s.nsrc;
+    J.out = s.out;
+    J.length = s.length;
+    J.bucket_base = nb;
+    nb += (s.length + cfg->bucket - 1) / cfg->bucket;
+    vec = vec && aligned(s.out, out_dtype == QSDP_BF16 ? 8 : 16);
+  }
+  tab.njobs = nj;
+  tab.total_buckets = nb;
+  tab.codes_vec = cvec ? 1 : 0;
+}
+
 qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg, int accumulate,
                         int divisor, int out_dtype, cudaStream_t stream, const DynSrc& dyn = DynSrc()) {
   if (out_dtype != QSDP_F32 && out_dtype != QSDP_F64 && out_dtype != QSDP_BF16)
@@ -186,43 +231,14 @@ qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg,
   int sms = 0;
   qsdp_status st = ensure_device(sms);
   if (st != QSDP_OK) return st;
+  for (const DJobSpec& s : jobs)
+    if (s.length > 0 && (s.nsrc < 1 || s.nsrc > 8)) return fail(QSDP_EINVAL, "nsrc must be in [1, 8]");
   size_t i = 0;
   while (i < jobs.size()) {
     DJobTable tab;
-    memset(&tab, 0, sizeof(tab));
-    tab.bits = cfg->bits;
-    tab.bucket = cfg->bucket;
-    tab.out_dtype = out_dtype;
-    tab.accumulate = accumulate;
-    tab.divisor = divisor < 1 ? 1 : divisor;
-    tab.parity_ptr = dyn.parity_ptr;
-    tab.parity_stride = dyn.parity_stride;
-    tab.parity_adj = dyn.parity_adj;
-    bool vec = cfg->bucket % 4 == 0;
-    bool cvec = cfg->bucket % 8 == 0;
-    int64_t nb = 0;
-    int nj = 0;
-    for (; i < jobs.size() && nj < kMaxJobs; ++i) {
-      const DJobSpec& s = jobs[i];
-      if (s.length <= 0) continue;
-      if (s.nsrc < 1 || s.nsrc > 8) return fail(QSDP_EINVAL, "nsrc must be in [1, 8]");
-      DJob& J = tab.jobs[nj++];
-      for (int p = 0; p < s.nsrc; ++p) {
-        J.codes[p] = s.codes[p];
-        J.meta[p] = s.meta[p];
-        cvec = cvec && aligned(s.codes[p], 8);
-      }
-      J.nsrc = s.nsrc;
-      J.out = s.out;
-      J.length = s.length;
-      J.bucket_base = nb;
-      nb += (s.length + cfg->bucket - 1) / cfg->bucket;
-      vec = vec && aligned(s.out, out_dtype == QSDP_BF16 ? 8 : 16);
-    }
-    tab.njobs = nj;
-    tab.total_buckets = nb;
-    tab.codes_vec = cvec ? 1 : 0;
-    if (nj == 0) continue;
+    bool vec = false;
+    build_dtab(tab, jobs, i, cfg, accumulate, divisor, out_dtype, dyn, vec);
+    if (tab.njobs == 0) continue;
     cudaError_t e = launch_dequant(tab, vec, sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "dequantize kernel launch");
   }
@@ -455,6 +471,7 @@ struct qsdp_comm {
   uint8_t* peer[QSDP_MAX_WORLD] = {};
   bool opened[QSDP_MAX_WORLD] = {};
   const unsigned long long* step_src = nullptr;
+  bool fused = true;  // single-launch collectives when the configuration allows
 
   static constexpr size_t kFlagBytes = 256;
   uint8_t* slot(uint8_t* b, int idx) const { return b + kFlagBytes + (size_t)idx * slot_bytes; }  // parity 0
@@ -514,7 +531,17 @@ qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32
     return cuda_fail(e, "cudaMemset(comm workspace)");
   }
   c->peer[rank] = c->base;
+  // fused single-launch collectives are opt-in until their pull phase is TMA-staged
+  // (measured slower than the 3-launch path in round 1)
+  const char* env = getenv("QSDP_FUSED");
+  c->fused = env != nullptr && env[0] == '1';
   *out = c;
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_comm_set_fused(qsdp_comm* c, int32_t enable) {
+  if (c == nullptr) return fail(QSDP_EINVAL, "null comm");
+  c->fused = enable != 0;
   return QSDP_OK;
 }
 
@@ -613,6 +640,50 @@ static QJobSpec comm_qjob(const void* x, const qsdp_segment& seg, uint8_t* slot,
   return q;
 }
 
+// The fused single-launch collective covers the hot configuration: fp32 input,
+// direct widths, buckets of 128..2048 elements, vector-aligned outputs.
+static bool fused_cfg_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
+  const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
+  return c->fused && in_dtype == QSDP_F32 && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 128 &&
+         cfg->bucket * 4 <= 8192;
+}
+
+static FuseSync comm_sync(const qsdp_comm* c) {
+  FuseSync fs;
+  memset(&fs, 0, sizeof(fs));
+  fs.epoch = c->epoch();
+  fs.arrive = reinterpret_cast<unsigned int*>(c->base + kEpochOff + 8);
+  fs.go = reinterpret_cast<unsigned long long*>(c->base + kEpochOff + 16);
+  for (int j = 0; j < c->world; ++j) fs.flags[j] = reinterpret_cast<unsigned long long*>(c->peer[j]);
+  fs.rank = c->rank;
+  fs.world = c->world;
+  return fs;
+}
+
+// Returns QSDP_OK if launched, QSDP_EINVAL (silently) if the fused path does not apply.
+static qsdp_status try_fused(qsdp_comm* c, const std::vector<QJobSpec>& q, const std::vector<DJobSpec>& d,
+                             const qsdp_qcfg* cfg, int accumulate, int divisor, int out_dtype, cudaStream_t s,
+                             bool& launched) {
+  launched = false;
+  for (int j = 0; j < c->world; ++j)
+    if (c->peer[j] == nullptr) return fail(QSDP_EPEER, "peers not opened");
+  QJobTable qt;
+  DJobTable dt;
+  size_t qi = 0, di = 0;
+  bool qvec = false, dvec = false;
+  build_qtab(qt, q, qi, cfg, nullptr, comm_dyn(c, 1), qvec);
+  build_dtab(dt, d, di, cfg, accumulate, divisor, out_dtype, comm_dyn(c, 0), dvec);
+  if (qi != q.size() || di != d.size() || !dvec || !dt.codes_vec) return QSDP_OK;
+  if (out_dtype != QSDP_F32 && !(out_dtype == QSDP_BF16 && !accumulate)) return QSDP_OK;
+  int sms = 0;
+  qsdp_status st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  cudaError_t e = launch_fused(qt, dt, comm_sync(c), sms, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fused collective launch");
+  launched = true;
+  return QSDP_OK;
+}
+
 qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, const qsdp_segment* segs,
                             const qsdp_key* key, void* full_out, int32_t out_dtype, void* stream) {
   if (c == nullptr || key == nullptr) return fail(QSDP_EINVAL, "null argument");
@@ -620,16 +691,7 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
   if (st != QSDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const qsdp_qcfg* cfg = &c->w;
-  // 1. quantize this rank's shard into its local slot (key worker 0, sharded.py:341)
   std::vector<QJobSpec> q(1, comm_qjob(shard, segs[c->rank], c->slot(c->base, 0), c->slot_codes, *key, 0));
-  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
-  if (st != QSDP_OK) return st;
-  // 2. publish + wait for every peer's slot of this call
-  if (c->world > 1) {
-    st = comm_barrier(c, s);
-    if (st != QSDP_OK) return st;
-  }
-  // 3. pull-dequantize all P shards over NVLink into the gathered buffer
   std::vector<DJobSpec> d(c->world);
   const size_t osz = dtype_size(out_dtype);
   for (int p = 0; p < c->world; ++p) {
@@ -641,6 +703,20 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
     d[p].length = segs[p].length;
     d[p].out = static_cast<uint8_t*>(full_out) + (size_t)(segs[p].global_start - segs[0].global_start) * osz;
   }
+  if (fused_cfg_ok(c, cfg, in_dtype)) {
+    bool launched = false;
+    st = try_fused(c, q, d, cfg, 0, 1, out_dtype, s, launched);
+    if (st != QSDP_OK || launched) return st;
+  }
+  // 1. quantize this rank's shard into its local slot (key worker 0, sharded.py:341)
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
+  if (st != QSDP_OK) return st;
+  // 2. publish + wait for every peer's slot of this call
+  if (c->world > 1) {
+    st = comm_barrier(c, s);
+    if (st != QSDP_OK) return st;
+  }
+  // 3. pull-dequantize all P shards over NVLink into the gathered buffer
   return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0));
 }
 
@@ -658,13 +734,6 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
     const void* x = static_cast<const uint8_t*>(full_grad) + (size_t)(segs[p].global_start - segs[0].global_start) * isz;
     q.push_back(comm_qjob(x, segs[p], c->slot(c->base, p), c->slot_codes, *key, (uint64_t)c->rank));
   }
-  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
-  if (st != QSDP_OK) return st;
-  if (c->world > 1) {
-    st = comm_barrier(c, s);
-    if (st != QSDP_OK) return st;
-  }
-  // 3. owner pulls its segment from sources 0..P-1 (in order) and accumulates
   std::vector<DJobSpec> d(1);
   memset(&d[0], 0, sizeof(DJobSpec));
   for (int p = 0; p < c->world; ++p) {
@@ -675,6 +744,18 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
   d[0].nsrc = c->world;
   d[0].length = segs[c->rank].length;
   d[0].out = shard_out;
+  if (fused_cfg_ok(c, cfg, in_dtype)) {
+    bool launched = false;
+    st = try_fused(c, q, d, cfg, 1, c->world, out_dtype, s, launched);
+    if (st != QSDP_OK || launched) return st;
+  }
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
+  if (st != QSDP_OK) return st;
+  if (c->world > 1) {
+    st = comm_barrier(c, s);
+    if (st != QSDP_OK) return st;
+  }
+  // 3. owner pulls its segment from sources 0..P-1 (in order) and accumulates
   return run_dequant(d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 0));
 }
 

@@ -180,6 +180,7 @@ struct JumpEntry {
 // Job tables for the batched kernels.
 // ---------------------------------------------------------------------------
 constexpr int kMaxJobs = 64;
+#define QSDP_FUSE_MAX_WORLD 8
 
 struct QJob {
   const void* x;          // segment input (element 0 of the segment)
@@ -233,6 +234,15 @@ struct DJobTable {
   int32_t parity_adj;
   const unsigned long long* parity_ptr;  // sources move by ((*p + adj) & 1) * parity_stride bytes
   int64_t parity_stride;
+};
+
+// Synchronisation words of a fused single-launch collective (see fused_collective_kernel).
+struct FuseSync {
+  unsigned long long* epoch;                       // local: collectives completed
+  unsigned int* arrive;                            // local: CTAs arrived in this launch
+  unsigned long long* go;                          // local: grid release flag (= target)
+  unsigned long long* flags[QSDP_FUSE_MAX_WORLD];  // flags[j] = rank j's flag array
+  int rank, world;
 };
 
 __host__ __device__ __forceinline__ int64_t payload_bytes(int64_t len, int bits) { return (len * bits + 7) / 8; }

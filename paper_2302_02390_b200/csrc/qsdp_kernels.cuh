@@ -636,9 +636,8 @@ struct JobCursor {
 };
 
 template <typename T, int INNER, int BITS, int NST>
-__global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_constant__ QJobTable tab) {
+__device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_t* smem) {
   const int64_t poff = q_parity_off(tab);
-  extern __shared__ __align__(128) uint8_t smem[];
   using Tr = InTraits<T>;
   using K = typename Tr::Key;
   constexpr uint32_t TOP = (1u << BITS) - 1u;
@@ -874,6 +873,12 @@ __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_con
   }
 }
 
+template <typename T, int INNER, int BITS, int NST>
+__global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_constant__ QJobTable tab) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  quantize_tma32_body<T, INNER, BITS, NST>(tab, smem);
+}
+
 // ---------------------------------------------------------------------------
 // K1/K2 for any width 1..16 (odd widths merge lane pairs into whole bytes),
 // S % 8 == 0.  Registers hold up to G groups per lane (HOLD) or the bucket is
@@ -1106,12 +1111,21 @@ __device__ __forceinline__ uint64_t load_group_bits_any(const uint8_t* p, int gi
   return bits == 16 ? v : (v & ((1ull << (4 * bits)) - 1ull));
 }
 
-template <int BITS>
+// COH: codes written earlier in the same launch (fused collectives) or by a
+// peer -- read at L2 (ld.global.cg), never through the non-coherent path.
+template <int BITS, bool COH = false>
 __device__ __forceinline__ uint64_t load_group_direct(const uint8_t* __restrict__ p, int gi) {
-  if (BITS == 8) return __ldg(reinterpret_cast<const uint32_t*>(p) + gi);
-  if (BITS == 4) return __ldg(reinterpret_cast<const uint16_t*>(p) + gi);
-  if (BITS == 16) return __ldg(reinterpret_cast<const unsigned long long*>(p) + gi);
-  return __ldg(p + gi);
+  if constexpr (COH) {
+    if (BITS == 8) return __ldcg(reinterpret_cast<const unsigned int*>(p) + gi);
+    if (BITS == 4) return __ldcg(reinterpret_cast<const unsigned short*>(p) + gi);
+    if (BITS == 16) return __ldcg(reinterpret_cast<const unsigned long long*>(p) + gi);
+    return __ldcg(reinterpret_cast<const unsigned char*>(p) + gi);
+  } else {
+    if (BITS == 8) return __ldg(reinterpret_cast<const uint32_t*>(p) + gi);
+    if (BITS == 4) return __ldg(reinterpret_cast<const uint16_t*>(p) + gi);
+    if (BITS == 16) return __ldg(reinterpret_cast<const unsigned long long*>(p) + gi);
+    return __ldg(p + gi);
+  }
 }
 
 __device__ __forceinline__ double code_to_double(uint32_t c) {
@@ -1160,12 +1174,11 @@ __device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, c
 // acc / P -- sharded.py:385-431).  Per-source scales of the current bucket are
 // staged in shared memory (one row per team) by lanes 0..nsrc-1.
 // BITS > 0: direct width with aligned group loads on full buckets; BITS == 0: any width.
-template <int BITS, int TL, int OUT, bool VEC, bool ACC>
-__global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJobTable tab) {
+template <int BITS, int TL, int OUT, bool VEC, bool ACC, bool COH = false>
+__device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_meta_base) {
   const int64_t poff = d_parity_off(tab);
   constexpr int TEAMS = 32 / TL;
   constexpr int U = 8;  // groups whose code words are loaded before use
-  __shared__ double sm_meta[ACC ? 8 : 1][ACC ? TEAMS : 1][8][3];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int lt = lane % TL;
@@ -1194,9 +1207,10 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
       double lo = 0.0, shift = 0.0, pitch = 0.0;
       if (active) {
         const float* m = meta_at(J.meta[0], poff) + 3 * lb;
-        shift = (double)m[0];
-        lo = (double)m[1];
-        pitch = __ddiv_rn(__dsub_rn((double)m[2], lo), top);  // QuantizedBlock.pitch
+        const float m0 = COH ? __ldcg(m) : m[0], m1 = COH ? __ldcg(m + 1) : m[1], m2 = COH ? __ldcg(m + 2) : m[2];
+        shift = (double)m0;
+        lo = (double)m1;
+        pitch = __ddiv_rn(__dsub_rn((double)m2, lo), top);  // QuantizedBlock.pitch
       }
       const uint8_t* __restrict__ cp = J.codes[0] + poff + lb * pbs;
       if (cvec && n == S) {
@@ -1205,7 +1219,7 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int gi = (g0 + u) * TL + lt;
-            w[u] = (g0 + u < gl && 4 * gi < n) ? load_group_direct<BITS>(cp, gi) : 0ull;
+            w[u] = (g0 + u < gl && 4 * gi < n) ? load_group_direct<BITS, COH>(cp, gi) : 0ull;
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -1238,13 +1252,14 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
       }
     } else {
       const int nsrc = J.nsrc;
-      double(*row)[3] = sm_meta[wib][team];
+      double(*row)[3] = reinterpret_cast<double(*)[3]>(sm_meta_base + ((size_t)(wib * TEAMS + team) * 8) * 3);
       if (active && lt < nsrc) {
         const float* m = meta_at(J.meta[lt], poff) + 3 * lb;
-        const double lo = (double)m[1];
+        const float m0 = COH ? __ldcg(m) : m[0], m1 = COH ? __ldcg(m + 1) : m[1], m2 = COH ? __ldcg(m + 2) : m[2];
+        const double lo = (double)m1;
         row[lt][0] = lo;
-        row[lt][1] = __ddiv_rn(__dsub_rn((double)m[2], lo), top);
-        row[lt][2] = (double)m[0];
+        row[lt][1] = __ddiv_rn(__dsub_rn((double)m2, lo), top);
+        row[lt][2] = (double)m0;
       }
       __syncwarp();
       constexpr int UA = 4;  // groups accumulated together (their code loads are in flight together)
@@ -1263,7 +1278,7 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
             const int e = 4 * gi;
             w[u] = 0;
             if (g0 + u < gl && e < n)
-              w[u] = (cvec && e + 4 <= n) ? load_group_direct<BITS>(cp, gi) : load_group_bits_any(cp, gi, bits, pb);
+              w[u] = (cvec && e + 4 <= n) ? load_group_direct<BITS, COH>(cp, gi) : load_group_bits_any(cp, gi, bits, pb);
           }
           const double lo = row[p][0], pitch = row[p][1], shift = row[p][2];
 #pragma unroll
@@ -1290,6 +1305,68 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
       __syncwarp();
     }
   }
+}
+
+template <int BITS, int TL, int OUT, bool VEC, bool ACC>
+__global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJobTable tab) {
+  __shared__ double sm_meta[ACC ? 8 * (32 / TL) * 8 * 3 : 1];
+  dequant_body<BITS, TL, OUT, VEC, ACC, false>(tab, sm_meta);
+}
+
+// ---------------------------------------------------------------------------
+// C1 / C2 as ONE persistent kernel per collective:
+//   phase A  quantize this rank's segments into its local slot(s) (TMA pipeline)
+//   barrier  grid-wide arrival (atomic counter) + cross-GPU flags over NVLink:
+//            the last CTA to arrive publishes `target` to every peer
+//            (st.release.sys), waits for all peers (ld.acquire.sys), advances the
+//            device epoch and releases the grid (go flag)
+//   phase C  pull-dequantize (C1) or ordered dequant-accumulate (C2) straight
+//            from the peers' slots over NVLink.
+// The grid is exactly the co-resident CTAs (persistent), so the in-kernel barrier
+// cannot deadlock.  World 1 uses the same kernel (grid barrier only).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void fused_barrier(const FuseSync& fs, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this CTA's phase-A codes are visible to peers and other CTAs
+    const unsigned int prev = atomicAdd(fs.arrive, 1u);
+    if (prev == gridDim.x - 1) {
+      *reinterpret_cast<volatile unsigned int*>(fs.arrive) = 0u;  // everyone arrived: reset for next launch
+      for (int j = 0; j < fs.world; ++j) {
+        if (j == fs.rank) continue;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fs.flags[j] + fs.rank), "l"(target) : "memory");
+      }
+      for (int j = 0; j < fs.world; ++j) {
+        if (j == fs.rank) continue;
+        unsigned long long v = 0;
+        do {
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(fs.flags[fs.rank] + j) : "memory");
+        } while (v < target);
+      }
+      *reinterpret_cast<volatile unsigned long long*>(fs.epoch) = target;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(fs.go), "l"(target) : "memory");
+    } else {
+      unsigned long long v = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(fs.go) : "memory");
+      } while (v < target);
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T, int INNER, int BITS, int NST, bool ACC, int OUT>
+__global__ void __launch_bounds__(256, 2) fused_collective_kernel(const __grid_constant__ QJobTable qt,
+                                                                  const __grid_constant__ DJobTable dt,
+                                                                  const __grid_constant__ FuseSync fs) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const unsigned long long target = ld_dev_u64(fs.epoch) + 1ull;
+  quantize_tma32_body<T, INNER, BITS, NST>(qt, smem);
+  fused_barrier(fs, target);
+  // the phase-A ring is free again: reuse its start for the per-source scale rows
+  dequant_body<BITS, 32, OUT, true, ACC, true>(dt, reinterpret_cast<double*>(smem));
 }
 
 // ---------------------------------------------------------------------------

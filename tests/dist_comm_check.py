@@ -23,11 +23,14 @@ def main():
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
     failures = 0
-    for size, bucket, wb, gb, pad in [(1 << 20, 1024, 8, 8, 1), (3 * 1024 * 1024 + 777, 1024, 8, 4, 1),
-                                      (1 << 22, 1024, 8, 8, 1024), (50000, 64, 6, 4, 1)]:
+    cases = [(1 << 20, 1024, 8, 8, 1, True), (3 * 1024 * 1024 + 777, 1024, 8, 4, 1, True),
+             (1 << 22, 1024, 8, 8, 1024, True), (1 << 22, 1024, 8, 8, 1024, False), (50000, 64, 6, 4, 1, True),
+             (200000, 256, 4, 2, 256, True), (200000, 512, 16, 8, 1, False)]
+    for size, bucket, wb, gb, pad, fused in cases:
         segs = plan_segments(size, world, pad)
         maxseg = max(n for _, n in segs)
         comm = QSDPComm(maxseg, QuantSpec(wb, bucket, "shift"), QuantSpec(gb, bucket, "uniform_stochastic"))
+        comm.set_fused(fused)
         rng = np.random.default_rng(size)
         full = (rng.standard_normal(size) * 0.02).astype(np.float32)
         grads = [(np.random.default_rng(size + 1 + p).standard_normal(size) * 1e-3).astype(np.float32)
@@ -54,7 +57,7 @@ def main():
             ok_rs = np.array_equal(sh[:n].cpu().numpy(), (acc / world).astype(np.float32))
             if not (ok_ag and ok_rs):
                 failures += 1
-                print(f"rank {rank} size {size} step {step}: ag {ok_ag} rs {ok_rs}", flush=True)
+                print(f"rank {rank} size {size} fused {fused} step {step}: ag {ok_ag} rs {ok_rs}", flush=True)
         # graph capture of one AG + RS with the step read on the device (epoch on device too)
         from paper_2302_02390_b200.quantize import advance_counter
         ctr = torch.zeros(1, dtype=torch.int64, device=dev)

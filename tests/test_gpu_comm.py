@@ -16,10 +16,12 @@ from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey
 pytestmark = pytest.mark.gpu
 
 
-def test_single_rank_comm_vs_oracle(oracle):
+@pytest.mark.parametrize("fused", [True, False])
+def test_single_rank_comm_vs_oracle(oracle, fused):
     dev = torch.device("cuda", 0)
     size = 3 * 1024 * 100 + 11
     comm = QSDPComm(size, QuantSpec(8, 1024, "shift"), QuantSpec(8, 1024, "uniform_stochastic"), device=dev)
+    comm.set_fused(fused)
     x = (np.random.default_rng(1).standard_normal(size) * 0.02).astype(np.float32)
     xt = torch.from_numpy(x).to(dev)
     for step in range(3):
@@ -36,12 +38,14 @@ def test_single_rank_comm_vs_oracle(oracle):
     comm.close()
 
 
-def test_graph_replay_with_device_step(oracle):
+@pytest.mark.parametrize("fused", [True, False])
+def test_graph_replay_with_device_step(oracle, fused):
     """A captured AG+RS replays with the step read on the device (fresh noise per replay)."""
     from paper_2302_02390_b200.quantize import advance_counter
     dev = torch.device("cuda", 0)
     size = 70000
     comm = QSDPComm(size, QuantSpec(8, 1024, "shift"), QuantSpec(4, 1024, "uniform_stochastic"), device=dev)
+    comm.set_fused(fused)
     ctr = torch.zeros(1, dtype=torch.int64, device=dev)
     comm.set_step_source(ctr)
     x = (np.random.default_rng(3).standard_normal(size) * 0.02).astype(np.float32)
