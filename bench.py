@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--out-dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gpt", action="store_true")
+    ap.add_argument("--gpt-steps", type=int, default=8)
+    ap.add_argument("--gpt-batch", type=int, default=8, help="sequences per GPU")
+    ap.add_argument("--gpt-seq", type=int, default=1024)
     return ap.parse_args()
 
 
@@ -419,6 +423,31 @@ def main():
                "path": "QSDPComm -> qsdp_all_gather / qsdp_reduce_scatter (C ABI), pinned host buffers, "
                        "one CUDA graph per step"}
 
+    # ---- GPT step/s: FSDP2 training step, unquantized (fp32 NCCL) vs QSDP comms ----
+    gpt = None
+    if not args.no_gpt:
+        try:
+            from paper_2302_02390_b200.gpt_train import build_model, run_training, shard_model
+            gpt = {"model": args.model, "batch_per_gpu": args.gpt_batch, "seq": args.gpt_seq,
+                   "data": "synthetic tokens", "timing": "CUDA events per step, max over ranks"}
+            for mode in ("fsdp", "qsdp"):
+                model = build_model(args.model, dev, seed=0)
+                ctx = shard_model(model, mode, wspec, gspec)
+                _, times = run_training(model, ctx, steps=args.gpt_steps, batch=args.gpt_batch, seq=args.gpt_seq,
+                                        warmup=2)
+                times = sorted(times)
+                med = times[len(times) // 2]
+                gpt[mode] = {"ms_per_step": round(med, 2), "steps_per_s": round(1e3 / med, 3)}
+                if ctx is not None:
+                    ctx.close()
+                del model
+                torch.cuda.empty_cache()
+            gpt["qsdp_speedup"] = round(gpt["fsdp"]["ms_per_step"] / gpt["qsdp"]["ms_per_step"], 3)
+            if world == 1:
+                gpt["note"] = "world 1: FSDP2 issues no collectives, both modes are identical"
+        except Exception as e:  # the GB/s metric stands on its own
+            gpt = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(args, world)
@@ -436,7 +465,7 @@ def main():
                        "parallelism": f"qsdp{world}", "execution": "one CUDA graph per step (device step counter), "
                                     + ("fused single-launch collectives" if comm_fused else "3 launches per collective"),
                        "convention": "sum over ranks of 4*N per collective / time"},
-            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
             "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
