@@ -189,6 +189,28 @@ __device__ __forceinline__ K team_max_k(K v) {
   for (int o = TL / 2; o > 0; o >>= 1) v = max(v, (K)__shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
+// Full-warp key reductions: redux.sync (one instruction) for 32-bit keys.
+template <typename K>
+__device__ __forceinline__ K warp_min_key(K v) {
+  if constexpr (sizeof(K) == 4) return (K)__reduce_min_sync(0xffffffffu, (int)v);
+  else return team_min_k<32>(v);
+}
+template <typename K>
+__device__ __forceinline__ K warp_max_key(K v) {
+  if constexpr (sizeof(K) == 4) return (K)__reduce_max_sync(0xffffffffu, (int)v);
+  else return team_max_k<32>(v);
+}
+
+// Pack four codes of width BITS (LSB-first).
+template <int BITS>
+__device__ __forceinline__ uint64_t pack4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+  if constexpr (BITS == 8) {
+    return __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+  } else {
+    return (uint64_t)c0 | ((uint64_t)c1 << BITS) | ((uint64_t)c2 << (2 * BITS)) | ((uint64_t)c3 << (3 * BITS));
+  }
+}
+
 template <int TL>
 __device__ __forceinline__ int team_min_i(int v) {
 #pragma unroll
@@ -705,16 +727,26 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
 
     // ---- pass 1: min/max keys (quantize.py:251-252) --------------------------
     K mnk = Tr::kMax, mxk = Tr::kMin;
-    if (in_smem) {
+    auto keys4 = [&](const T v[4]) {
+      const K k0 = Tr::key(v[0]), k1 = Tr::key(v[1]), k2 = Tr::key(v[2]), k3 = Tr::key(v[3]);
+      mnk = min(min(mnk, k0), min(k1, min(k2, k3)));
+      mxk = max(max(mxk, k0), max(k1, max(k2, k3)));
+    };
+    if (in_smem && (S & 127) == 0) {
+      const int gfull = S >> 7;
 #pragma unroll 4
+      for (int g = 0; g < gfull; ++g) {
+        T v[4];
+        lds_group(sb, 4 * (g * 32 + lane), v);
+        keys4(v);
+      }
+    } else if (in_smem) {
       for (int g = 0; g < gl; ++g) {
         const int e = 4 * (g * 32 + lane);
         if (e < n) {
           T v[4];
           lds_group(sb, e, v);
-          const K k0 = Tr::key(v[0]), k1 = Tr::key(v[1]), k2 = Tr::key(v[2]), k3 = Tr::key(v[3]);
-          mnk = min(min(mnk, k0), min(k1, min(k2, k3)));
-          mxk = max(max(mxk, k0), max(k1, max(k2, k3)));
+          keys4(v);
         }
       }
     } else {
@@ -732,8 +764,8 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
         }
       }
     }
-    mnk = team_min_k<32>(mnk);
-    mxk = team_max_k<32>(mxk);
+    mnk = warp_min_key(mnk);
+    mxk = warp_max_key(mxk);
     const bool nonfinite = n > 0 && !(Tr::kNegInf < mnk && mxk < Tr::kPosInf);
     const T mnv = Tr::from_key(mnk), mxv = Tr::from_key(mxk);
     const float lof = nonfinite ? 0.0f : (float)Tr::to_d(mnv);
@@ -759,33 +791,46 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
       if (INNER == 0) {
         shift_f = __double2float_rn(__dmul_rn(r, span));  // _f32(r*(hi-lo))
         const double C = __dsub_rn(kMagic + 0.5, __dmul_rn(r, top));
+        // A certified code lies in [0, top]: the low 19 integer bits are the code.
+        auto code4 = [&](const T v[4], uint32_t c[4]) -> bool {
+          bool unc = false;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            double a = __dsub_rn(Tr::to_d(v[i]), lo);
+            if constexpr (sizeof(T) == 8) a = fmin(fmax(a, 0.0), span);  // == np.clip of u
+            const double y = __fma_rn(a, K1, C);
+            const uint32_t fr = (uint32_t)__double2loint(y);
+            unc |= (fr + 2u) <= 4u;  // |frac - 1/2| <= 2 units: not certified
+            c[i] = (uint32_t)__double2hiint(y) & 0x7FFFFu;
+          }
+          return unc;
+        };
+        auto fix4 = [&](const T v[4], uint32_t c[4]) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) c[i] = exact_shift_code(__dsub_rn(Tr::to_d(v[i]), lo), span, r, pitch, top);
+        };
+        if ((S & 127) == 0) {  // every lane owns exactly S/128 full groups
+          const int gfull = S >> 7;
 #pragma unroll 2
-        for (int g = 0; g < gl; ++g) {
-          const int gi = g * 32 + lane;
-          const int e = 4 * gi;
-          if (e < n) {
+          for (int g = 0; g < gfull; ++g) {
+            const int gi = g * 32 + lane;
             T v[4];
-            lds_group(sb, e, v);
+            lds_group(sb, 4 * gi, v);
             uint32_t c[4];
-            bool unc = false;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              double a = __dsub_rn(Tr::to_d(v[i]), lo);
-              if constexpr (sizeof(T) == 8) a = fmin(fmax(a, 0.0), span);  // == np.clip of u
-              const double y = __fma_rn(a, K1, C);
-              const uint32_t fr = (uint32_t)__double2loint(y);
-              const int ip = (int)((uint32_t)__double2hiint(y) & 0xFFFFFu) - (1 << 19);
-              unc |= (fr + 2u) <= 4u;  // |frac - 1/2| <= 2 units: not certified
-              c[i] = (uint32_t)min(max(ip, 0), (int)TOP);
+            if (code4(v, c)) fix4(v, c);
+            store_direct<BITS>(cbase, gi, pack4<BITS>(c[0], c[1], c[2], c[3]), 0, true);
+          }
+        } else {
+          for (int g = 0; g < gl; ++g) {
+            const int gi = g * 32 + lane;
+            const int e = 4 * gi;
+            if (e < n) {
+              T v[4];
+              lds_group(sb, e, v);
+              uint32_t c[4];
+              if (code4(v, c)) fix4(v, c);
+              store_direct<BITS>(cbase, gi, pack4<BITS>(c[0], c[1], c[2], c[3]), 0, true);
             }
-            if (unc) {
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                c[i] = exact_shift_code(__dsub_rn(Tr::to_d(v[i]), lo), span, r, pitch, top);
-            }
-            const uint64_t w = (uint64_t)c[0] | ((uint64_t)c[1] << BITS) | ((uint64_t)c[2] << (2 * BITS)) |
-                               ((uint64_t)c[3] << (3 * BITS));
-            store_direct<BITS>(cbase, gi, w, 0, true);
           }
         }
       } else if (BITS != 16 && (S & 255) == 0) {
