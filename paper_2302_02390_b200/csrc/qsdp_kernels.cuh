@@ -1219,6 +1219,72 @@ __device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, c
 // acc / P -- sharded.py:385-431).  Per-source scales of the current bucket are
 // staged in shared memory (one row per team) by lanes 0..nsrc-1.
 // BITS > 0: direct width with aligned group loads on full buckets; BITS == 0: any width.
+// One warp per bucket, S % 128 == 0 (every lane owns S/128 full groups of 4).
+// ADD0: K4 with a single source and divisor 1 -- out = (0.0 + val) / 1 (the
+// reference's zeros + vals; only the sign of a zero can differ from val).
+template <int BITS, int OUT, bool COH, bool ADD0 = false>
+__device__ __forceinline__ void dequant_fast32(const DJobTable& tab, int64_t poff, int64_t warp, int64_t nwarps) {
+  constexpr int UMAX = 8;
+  const int lane = threadIdx.x & 31;
+  const int S = tab.bucket;
+  const int G = S >> 7;  // groups per lane
+  const double top = (double)((1u << BITS) - 1u);
+  const int64_t pbs = payload_bytes(S, BITS);
+  struct Pre {
+    uint32_t w[UMAX];
+    float m0, m1, m2;
+    int j, n;
+    int64_t lb;
+  };
+  auto fetch = [&](int64_t b, Pre& p) {
+    const int j = find_job_d(tab, b);
+    const DJob& J = tab.jobs[j];
+    p.j = j;
+    p.lb = b - J.bucket_base;
+    p.n = (int)min((int64_t)S, J.length - p.lb * S);
+    const float* m = meta_at(J.meta[0], poff) + 3 * p.lb;
+    p.m0 = COH ? __ldcg(m) : m[0];
+    p.m1 = COH ? __ldcg(m + 1) : m[1];
+    p.m2 = COH ? __ldcg(m + 2) : m[2];
+    const uint8_t* __restrict__ cp = J.codes[0] + poff + p.lb * pbs;
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u) {
+      const int gi = u * 32 + lane;
+      p.w[u] = (u < G && 4 * gi < p.n) ? (uint32_t)load_group_direct<BITS, COH>(cp, gi) : 0u;
+    }
+  };
+  int64_t b = warp;
+  if (b >= tab.total_buckets) return;
+  Pre cur;
+  fetch(b, cur);
+  while (b < tab.total_buckets) {
+    const int64_t bn = b + nwarps;
+    Pre nxt;
+    if (bn < tab.total_buckets) fetch(bn, nxt);  // issued before the current bucket's math
+    const DJob& J = tab.jobs[cur.j];
+    const double lo = (double)cur.m1, shift = (double)cur.m0;
+    const double pitch = __ddiv_rn(__dsub_rn((double)cur.m2, lo), top);  // QuantizedBlock.pitch
+    const int64_t off = cur.lb * S;
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u) {
+      const int gi = u * 32 + lane;
+      const int e = 4 * gi;
+      if (u < G && e < cur.n) {
+        double v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double c = code_to_double((cur.w[u] >> (i * BITS)) & ((1u << BITS) - 1u));
+          v[i] = __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift);  // (lo + code*pitch) + shift
+          if (ADD0) v[i] = __dadd_rn(0.0, v[i]);
+        }
+        store_out4<OUT, true>(J.out, off + e, cur.n - e, v);
+      }
+    }
+    b = bn;
+    cur = nxt;
+  }
+}
+
 template <int BITS, int TL, int OUT, bool VEC, bool ACC, bool COH = false>
 __device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_meta_base) {
   const int64_t poff = d_parity_off(tab);
@@ -1238,6 +1304,20 @@ __device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_me
   const int gl = (groups + TL - 1) / TL;
   const uint64_t cmask = (1ull << bits) - 1ull;
   const bool cvec = BITS > 0 && tab.codes_vec;
+
+  if constexpr (TL == 32 && (BITS == 8 || BITS == 4) && VEC) {
+    // K3 hot path: a bucket's code words are loaded one bucket AHEAD (software
+    // pipelining across the warp's buckets), so HBM / NVLink latency overlaps the
+    // previous bucket's fp64 dequantization.  K4 with one source takes it too.
+    bool single = !ACC || tab.divisor == 1;
+    if constexpr (ACC) {
+      for (int j = 0; j < tab.njobs && single; ++j) single = tab.jobs[j].nsrc == 1;
+    }
+    if (single && cvec && (S & 127) == 0 && S <= 1024) {
+      dequant_fast32<BITS, OUT, COH, ACC>(tab, poff, warp, nwarps);
+      return;
+    }
+  }
 
   for (int64_t b0 = warp * TEAMS; b0 < tab.total_buckets; b0 += nwarps * TEAMS) {
     const int64_t b = b0 + team;
