@@ -89,6 +89,12 @@ __host__ __device__ __forceinline__ U128 mad128(U128 a, U128 b, U128 c) { return
 
 __host__ __device__ __forceinline__ U128 pcg_mult() { return U128{PCG_MULT_LO, PCG_MULT_HI}; }
 
+// One PCG64 LCG step  s <- s*M + inc (mod 2^128).  (A hand-written 32-bit-limb
+// mad.cc carry chain was measured no faster: SASS has no carry-out IMAD, so each
+// partial product becomes IMAD + IADD3; the 64-bit form below lets ptxas use
+// IMAD.WIDE.U32 pairs.)
+__host__ __device__ __forceinline__ U128 pcg_step(U128 s, U128 inc) { return add128(mul128(s, pcg_mult()), inc); }
+
 // Finish SeedSequence for one bucket and seed PCG64; returns (state, inc).
 __host__ __device__ __forceinline__ void seed_bucket(const SeedPrefix& pre, uint64_t start, U128& state,
                                                      U128& inc) {

@@ -282,7 +282,7 @@ struct Coder {
     }
   }
 
-  __device__ __forceinline__ void step() { st = mad128(st, pcg_mult(), inc); }
+  __device__ __forceinline__ void step() { st = pcg_step(st, inc); }
   __device__ __forceinline__ void jump() { st = add128(mul128(jmp_a, st), jmp_c); }
 
   // 4 codes of group starting at element e (elements >= n coded 0), packed LSB-first.
@@ -601,7 +601,7 @@ static __device__ __noinline__ uint64_t stoch_octet_exact(const T* v, U128 st, U
     uint32_t c = ip + (fq > dh ? 1u : 0u);
     if ((fq - dh) <= 1u) c = exact_stoch_code(__dsub_rn(Tr::to_d(v[i]), lo), span, top, st);
     w |= (uint64_t)c << (i * BITS);
-    st = mad128(st, pcg_mult(), inc);
+    st = pcg_step(st, inc);
   }
   return w;
 }
@@ -862,7 +862,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             const uint32_t dh = pcg_output_hi32(st);
             unc |= (fq - dh) <= 1u;  // the only uncertain case
             w |= (uint64_t)(ip + (fq > dh ? 1u : 0u)) << (i * BITS);
-            if (i < 7) st = mad128(st, pcg_mult(), inc);
+            if (i < 7) st = pcg_step(st, inc);
           }
           if (unc) w = stoch_octet_exact<T, BITS>(sb + 8 * o, st0, inc, lo, span, K1, top);
           store_octet<BITS>(cbase, o, w);
@@ -895,7 +895,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
               const bool unc = (fq - dh) <= 1u;
               if (unc) c = exact_stoch_code(__dsub_rn(Tr::to_d(v[i]), lo), span, top, st);
               w |= (uint64_t)c << (i * BITS);
-              if (i < 3) st = mad128(st, pcg_mult(), inc);
+              if (i < 3) st = pcg_step(st, inc);
             }
             st = add128(mul128(JA, st), jc);
             store_direct<BITS>(cbase, gi, w, 0, true);
@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
     if (!degenerate) {
       seed_bucket(q_seed(tab, J), (uint64_t)(J.global_start + br.off), st, inc);
       if (INNER == 0) {
-        st = mad128(st, pcg_mult(), inc);
+        st = pcg_step(st, inc);
         const double d = u64_to_unit_double(pcg_output(st));
         r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));
         shift_f = __double2float_rn(__dmul_rn(r, span));
@@ -1120,7 +1120,7 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
         if (INNER == 0) {
           code = exact_shift_code(a, span, r, pitch, top);
         } else {
-          st = mad128(st, pcg_mult(), inc);
+          st = pcg_step(st, inc);
           code = exact_stoch_code(a, span, top, st);
         }
       }
