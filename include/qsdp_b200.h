@@ -22,6 +22,10 @@
  *   encode  wire.py:108-131                            qsdp_wire_encode (host export of one segment)
  *   ShardedMLP._gather  sharded.py:323-373             qsdp_all_gather (one process per GPU)
  *   ShardedMLP._reduce_scatter  sharded.py:375-433     qsdp_reduce_scatter
+ *   quantize_bucket (levels) + quantize_with_levels    qsdp_quantize_levels / _batch
+ *     quantize.py:235-286, 400-416                       (inner = QSDP_INNER_LEVELS)
+ *   dequantize(block, "levels", table)  quantize.py:225-231  qsdp_dequantize_levels / _batch
+ *   learn_levels  quantize.py:366-397                  qsdp_learn_levels (one sequential pass)
  *
  * Device layout of one quantized segment (length L, bucket S, width b):
  *   codes: bucket j's LSB-first packed codes at byte j*ceil(S*b/8), each bucket
@@ -57,7 +61,7 @@ typedef enum {
   QSDP_EPEER = 6
 } qsdp_status;
 
-typedef enum { QSDP_INNER_SHIFT = 0, QSDP_INNER_STOCHASTIC = 1 } qsdp_inner;
+typedef enum { QSDP_INNER_SHIFT = 0, QSDP_INNER_STOCHASTIC = 1, QSDP_INNER_LEVELS = 2 } qsdp_inner;
 typedef enum { QSDP_NOISE_PCG64_SEEDSEQ = 0 } qsdp_noise;
 typedef enum { QSDP_F32 = 0, QSDP_F64 = 1, QSDP_BF16 = 2 } qsdp_dtype;
 
@@ -144,6 +148,34 @@ qsdp_status qsdp_dequant_accumulate(const uint8_t* const* codes, const float* co
 qsdp_status qsdp_dequant_accumulate_batch(const qsdp_ditem* items, int32_t nitems,
                                           const qsdp_qcfg* cfg, int32_t divisor,
                                           int32_t out_dtype, void* stream);
+
+/* ---- learned levels ----
+ * d_levels: device float64[nlevels], strictly increasing (LevelTable,
+ * quantize.py:344-363).  cfg->inner must be QSDP_INNER_LEVELS; the keys are not
+ * used (levels mode draws no noise); meta shift is 0.  Codes are bit-exact with
+ * quantize_with_levels(clip((v-lo)/(hi-lo), 0, 1), table) (searchsorted over the
+ * level mids, side="left").  Quantize takes any power-of-two table with
+ * nlevels <= 2^bits (a wider table is EINVAL: its codes could not be stored). */
+qsdp_status qsdp_quantize_levels_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
+                                       const qsdp_qcfg* cfg, const double* d_levels, int32_t nlevels,
+                                       uint64_t* d_bad, void* stream);
+qsdp_status qsdp_quantize_levels(const void* x, int32_t x_dtype, int64_t length, const qsdp_qcfg* cfg,
+                                 const double* d_levels, int32_t nlevels, uint8_t* codes, float* meta,
+                                 uint64_t* d_bad, void* stream);
+/* lo + levels[code] * (hi - lo) in fp64, stored as out_dtype; nlevels == 2^bits
+   ("level table size does not match bit_width" otherwise) */
+qsdp_status qsdp_dequantize_levels_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
+                                         const double* d_levels, int32_t nlevels, int32_t out_dtype,
+                                         void* stream);
+qsdp_status qsdp_dequantize_levels(const uint8_t* codes, const float* meta, int64_t length,
+                                   const qsdp_qcfg* cfg, const double* d_levels, int32_t nlevels, void* out,
+                                   int32_t out_dtype, void* stream);
+/* One pass of learn_levels over device float64 values[n] (in order), updating
+ * d_levels[nlevels] in place, including the re-sort / collision nudge.  The
+ * caller performs the reference's empty / non-finite / distinct-count checks.
+ * nlevels: a power of two <= 4096. */
+qsdp_status qsdp_learn_levels(const double* d_values, int64_t n, double* d_levels, int32_t nlevels,
+                              double learning_rate, void* stream);
 
 /* ---- host wire export (wire.py:108-131): codes/meta already on the host ---- */
 int64_t qsdp_wire_encode(const uint8_t* codes, const float* meta, int64_t length,

@@ -78,6 +78,14 @@ def lib():
         L.qo_message_size_bits.restype = i64
         L.qo_encode_segment.argtypes = [vp, vp, i64, i64, i32, vp]
         L.qo_encode_segment.restype = i64
+        dbl = ctypes.c_double
+        L.qo_level_code.argtypes = [dbl, vp, i64]
+        L.qo_level_code.restype = ctypes.c_uint32
+        L.qo_quantize_levels_segment.argtypes = [vp, i64, i64, i32, vp, vp, vp]
+        L.qo_quantize_levels_segment.restype = i64
+        L.qo_dequantize_levels_segment.argtypes = [vp, vp, i64, i64, i32, vp, vp]
+        L.qo_dequantize_levels_segment.restype = i32
+        L.qo_learn_levels.argtypes = [vp, i64, vp, i64, dbl]
         _lib = L
     return _lib
 
@@ -168,6 +176,54 @@ def unpack(codes, length, bits) -> np.ndarray:
     out = np.zeros(max(length, 1), dtype=np.uint32)
     lib().qo_unpack(_ptr(codes), length, bits, _ptr(out))
     return out[:length]
+
+
+# -- learned levels (quantize.py:344-422) -----------------------------------------
+
+
+def level_codes(u, levels) -> np.ndarray:
+    """quantize_with_levels(u, LevelTable(levels), stochastic=False)."""
+    q = np.ascontiguousarray(levels, dtype=np.float64)
+    return np.array([lib().qo_level_code(float(x), _ptr(q), q.size) for x in np.atleast_1d(u)],
+                    dtype=np.uint32)
+
+
+def quantize_levels_segment(x, bucket, bits, levels):
+    """bucketed_quantize(x, bucket, bits, "levels", levels=table) + packing.
+    Returns (packed codes, meta float32[nb, 3], bad_index)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    q = np.ascontiguousarray(levels, dtype=np.float64)
+    assert q.size == 1 << bits
+    n = x.size
+    codes = np.zeros(max(codes_bytes(n, bucket, bits), 1), dtype=np.uint8)
+    meta = np.zeros((max(num_buckets(n, bucket), 1), 3), dtype=np.float32)
+    bad = lib().qo_quantize_levels_segment(_ptr(x), n, bucket, bits, _ptr(q), _ptr(codes), _ptr(meta))
+    return codes[: codes_bytes(n, bucket, bits)], meta[: num_buckets(n, bucket)], int(bad)
+
+
+def dequantize_levels_segment(codes, meta, length, bucket, bits, levels) -> np.ndarray:
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    meta = np.ascontiguousarray(meta, dtype=np.float32)
+    q = np.ascontiguousarray(levels, dtype=np.float64)
+    out = np.zeros(max(length, 1), dtype=np.float64)
+    if lib().qo_dequantize_levels_segment(_ptr(codes), _ptr(meta), length, bucket, bits, _ptr(q), _ptr(out)):
+        raise ValueError("nonzero padding bits in payload")
+    return out[:length]
+
+
+def learn_levels(values, initial, lr=0.01) -> np.ndarray:
+    """learn_levels(values, LevelTable(initial), lr).levels, including the
+    distinct-count early return (quantize.py:366-397)."""
+    v = np.ascontiguousarray(np.atleast_1d(values), dtype=np.float64)
+    q = np.array(initial, dtype=np.float64)
+    if v.size == 0:
+        raise ValueError("cannot learn levels from an empty value set")
+    if not np.all(np.isfinite(v)):
+        raise ValueError("non-finite value")
+    if np.unique(v).size < q.size:
+        return q
+    lib().qo_learn_levels(_ptr(v), v.size, _ptr(q), q.size, float(lr))
+    return q
 
 
 # -- protocol (sharded.py) -------------------------------------------------------

@@ -24,6 +24,7 @@ QSDP_EPEER = 6
 
 INNER_SHIFT = 0
 INNER_STOCHASTIC = 1
+INNER_LEVELS = 2
 F32, F64, BF16 = 0, 1, 2
 IPC_HANDLE_BYTES = 64
 MAX_WORLD = 8
@@ -35,6 +36,8 @@ EXPORTED_SYMBOLS = (
     "qsdp_wire_encode", "qsdp_comm_create", "qsdp_comm_ipc_handle", "qsdp_comm_open_peers",
     "qsdp_all_gather", "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_batch_dstep",
     "qsdp_counter_add", "qsdp_comm_set_step_source", "qsdp_comm_set_fused",
+    "qsdp_quantize_levels", "qsdp_quantize_levels_batch", "qsdp_dequantize_levels",
+    "qsdp_dequantize_levels_batch", "qsdp_learn_levels",
 )
 
 
@@ -118,11 +121,18 @@ def lib():
     L.qsdp_all_gather.argtypes = [vp, vp, i32, segp, keyp, vp, i32, vp]
     L.qsdp_reduce_scatter.argtypes = [vp, vp, i32, segp, keyp, vp, i32, vp]
     L.qsdp_comm_destroy.argtypes = [vp]
+    L.qsdp_quantize_levels.argtypes = [vp, i32, i64, cfgp, vp, i32, vp, vp, vp, vp]
+    L.qsdp_quantize_levels_batch.argtypes = [ctypes.POINTER(QItem), i32, i32, cfgp, vp, i32, vp, vp]
+    L.qsdp_dequantize_levels.argtypes = [vp, vp, i64, cfgp, vp, i32, vp, i32, vp]
+    L.qsdp_dequantize_levels_batch.argtypes = [ctypes.POINTER(DItem), i32, cfgp, vp, i32, i32, vp]
+    L.qsdp_learn_levels.argtypes = [vp, i64, vp, i32, ctypes.c_double, vp]
     for name in ("qsdp_quantize", "qsdp_quantize_batch", "qsdp_quantize_batch_dstep", "qsdp_counter_add",
                  "qsdp_comm_set_step_source", "qsdp_comm_set_fused", "qsdp_dequantize", "qsdp_dequantize_batch",
                  "qsdp_dequant_accumulate", "qsdp_dequant_accumulate_batch", "qsdp_comm_create",
                  "qsdp_comm_ipc_handle", "qsdp_comm_open_peers", "qsdp_all_gather",
-                 "qsdp_reduce_scatter", "qsdp_comm_destroy"):
+                 "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_levels",
+                 "qsdp_quantize_levels_batch", "qsdp_dequantize_levels", "qsdp_dequantize_levels_batch",
+                 "qsdp_learn_levels"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib

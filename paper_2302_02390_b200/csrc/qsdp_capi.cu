@@ -35,6 +35,10 @@ cudaError_t upload_jump_f32(const JumpEntry* host);
 cudaError_t upload_jump_f64(const JumpEntry* host);
 cudaError_t upload_jump_fused(const JumpEntry* host);
 cudaError_t launch_fused(const QJobTable& qt, const DJobTable& dt, const FuseSync& fs, int sms, cudaStream_t s);
+cudaError_t launch_quantize_levels(const QJobTable& tab, int in_f64, const double* levels, int nl, int sms,
+                                   cudaStream_t s);
+cudaError_t launch_dequant_levels(const DJobTable& tab, const double* levels, int sms, cudaStream_t s);
+cudaError_t launch_learn_levels(const double* values, int64_t n, double* q, int nl, double lr, cudaStream_t s);
 }  // namespace qsdp
 
 using namespace qsdp;
@@ -95,12 +99,12 @@ SeedPrefix key_prefix(const qsdp_key& k, uint64_t worker) {
   return make_prefix(k.root_seed, k.step, k.layer, k.phase, worker);
 }
 
-qsdp_status check_cfg(const qsdp_qcfg* c) {
+qsdp_status check_cfg(const qsdp_qcfg* c, bool levels = false) {
   if (c == nullptr) return fail(QSDP_EINVAL, "null qsdp_qcfg");
   if (c->bits < 1 || c->bits > 16) return fail(QSDP_EINVAL, "bit_width must be in [1, 16]");
   if (c->bucket < 1) return fail(QSDP_EINVAL, "bucket_size must be >= 1");
-  if (c->inner != QSDP_INNER_SHIFT && c->inner != QSDP_INNER_STOCHASTIC)
-    return fail(QSDP_EINVAL, "unknown inner mode");
+  if (levels ? c->inner != QSDP_INNER_LEVELS : (c->inner != QSDP_INNER_SHIFT && c->inner != QSDP_INNER_STOCHASTIC))
+    return fail(QSDP_EINVAL, levels ? "levels entry points take inner = QSDP_INNER_LEVELS" : "unknown inner mode");
   if (c->noise != QSDP_NOISE_PCG64_SEEDSEQ) return fail(QSDP_EINVAL, "unsupported noise mode");
   return QSDP_OK;
 }
@@ -162,7 +166,8 @@ void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, co
 }
 
 qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const qsdp_qcfg* cfg,
-                         uint64_t* d_bad, cudaStream_t stream, const DynSrc& dyn = DynSrc()) {
+                         uint64_t* d_bad, cudaStream_t stream, const DynSrc& dyn = DynSrc(),
+                         const double* levels = nullptr, int nlevels = 0) {
   if (x_dtype != QSDP_F32 && x_dtype != QSDP_F64) return fail(QSDP_EINVAL, "input dtype must be f32 or f64");
   int sms = 0;
   qsdp_status st = ensure_device(sms);
@@ -173,8 +178,9 @@ qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const q
     bool vec = false;
     build_qtab(tab, jobs, i, cfg, d_bad, dyn, vec);
     if (tab.njobs == 0) continue;
-    cudaError_t e = x_dtype == QSDP_F64 ? launch_quantize_f64(tab, vec, sms, stream)
-                                         : launch_quantize_f32(tab, vec, sms, stream);
+    cudaError_t e = levels != nullptr      ? launch_quantize_levels(tab, x_dtype == QSDP_F64, levels, nlevels, sms, stream)
+                    : x_dtype == QSDP_F64 ? launch_quantize_f64(tab, vec, sms, stream)
+                                          : launch_quantize_f32(tab, vec, sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "quantize kernel launch");
   }
   return QSDP_OK;
@@ -225,7 +231,8 @@ void build_dtab(DJobTable& tab, const std::vector<DJobSpec>& jobs, size_t& i, co
 }
 
 qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg, int accumulate,
-                        int divisor, int out_dtype, cudaStream_t stream, const DynSrc& dyn = DynSrc()) {
+                        int divisor, int out_dtype, cudaStream_t stream, const DynSrc& dyn = DynSrc(),
+                        const double* levels = nullptr) {
   if (out_dtype != QSDP_F32 && out_dtype != QSDP_F64 && out_dtype != QSDP_BF16)
     return fail(QSDP_EINVAL, "output dtype must be f32, f64 or bf16");
   int sms = 0;
@@ -239,7 +246,8 @@ qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg,
     bool vec = false;
     build_dtab(tab, jobs, i, cfg, accumulate, divisor, out_dtype, dyn, vec);
     if (tab.njobs == 0) continue;
-    cudaError_t e = launch_dequant(tab, vec, sms, stream);
+    cudaError_t e = levels != nullptr ? launch_dequant_levels(tab, levels, sms, stream)
+                                      : launch_dequant(tab, vec, sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "dequantize kernel launch");
   }
   return QSDP_OK;
@@ -299,10 +307,10 @@ qsdp_status qsdp_quantize_batch(const qsdp_qitem* items, int32_t nitems, int32_t
   return qsdp_quantize_batch_dstep(items, nitems, x_dtype, cfg, d_bad, nullptr, stream);
 }
 
-qsdp_status qsdp_quantize_batch_dstep(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
-                                      const qsdp_qcfg* cfg, uint64_t* d_bad, const uint64_t* d_step,
-                                      void* stream) {
-  qsdp_status st = check_cfg(cfg);
+static qsdp_status quantize_items(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype, const qsdp_qcfg* cfg,
+                                  uint64_t* d_bad, const uint64_t* d_step, const double* levels, int nlevels,
+                                  void* stream) {
+  qsdp_status st = check_cfg(cfg, levels != nullptr);
   if (st != QSDP_OK) return st;
   if (nitems < 0 || (nitems > 0 && items == nullptr)) return fail(QSDP_EINVAL, "bad item list");
   std::vector<QJobSpec> jobs;
@@ -331,7 +339,37 @@ qsdp_status qsdp_quantize_batch_dstep(const qsdp_qitem* items, int32_t nitems, i
   }
   DynSrc dyn;
   dyn.step_ptr = reinterpret_cast<const unsigned long long*>(d_step);
-  return run_quantize(jobs, x_dtype, cfg, d_bad, reinterpret_cast<cudaStream_t>(stream), dyn);
+  return run_quantize(jobs, x_dtype, cfg, d_bad, reinterpret_cast<cudaStream_t>(stream), dyn, levels, nlevels);
+}
+
+qsdp_status qsdp_quantize_batch_dstep(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
+                                      const qsdp_qcfg* cfg, uint64_t* d_bad, const uint64_t* d_step,
+                                      void* stream) {
+  return quantize_items(items, nitems, x_dtype, cfg, d_bad, d_step, nullptr, 0, stream);
+}
+
+static bool pow2(int64_t v) { return v >= 1 && (v & (v - 1)) == 0; }
+
+qsdp_status qsdp_quantize_levels_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
+                                       const qsdp_qcfg* cfg, const double* d_levels, int32_t nlevels,
+                                       uint64_t* d_bad, void* stream) {
+  if (d_levels == nullptr) return fail(QSDP_EINVAL, "inner 'levels' requires a LevelTable");
+  if (!pow2(nlevels)) return fail(QSDP_EINVAL, "level count must be a power of two");
+  if (cfg != nullptr && cfg->bits >= 1 && cfg->bits <= 16 && nlevels > (1 << cfg->bits))
+    return fail(QSDP_EINVAL, "code out of range for bit_width: level table larger than 2**bits");
+  return quantize_items(items, nitems, x_dtype, cfg, d_bad, nullptr, d_levels, nlevels, stream);
+}
+
+qsdp_status qsdp_quantize_levels(const void* x, int32_t x_dtype, int64_t length, const qsdp_qcfg* cfg,
+                                 const double* d_levels, int32_t nlevels, uint8_t* codes, float* meta,
+                                 uint64_t* d_bad, void* stream) {
+  qsdp_qitem it;
+  memset(&it, 0, sizeof(it));
+  it.x = x;
+  it.seg.length = length;
+  it.codes = codes;
+  it.meta = meta;
+  return qsdp_quantize_levels_batch(&it, 1, x_dtype, cfg, d_levels, nlevels, d_bad, stream);
 }
 
 qsdp_status qsdp_dequantize(const uint8_t* codes, const float* meta, int64_t length, const qsdp_qcfg* cfg,
@@ -347,8 +385,9 @@ qsdp_status qsdp_dequantize(const uint8_t* codes, const float* meta, int64_t len
 }
 
 static qsdp_status dequant_items(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg, int acc,
-                                 int32_t divisor, int32_t out_dtype, void* stream) {
-  qsdp_status st = check_cfg(cfg);
+                                 int32_t divisor, int32_t out_dtype, void* stream,
+                                 const double* levels = nullptr) {
+  qsdp_status st = check_cfg(cfg, levels != nullptr);
   if (st != QSDP_OK) return st;
   std::vector<DJobSpec> jobs;
   jobs.reserve(nitems);
@@ -367,7 +406,41 @@ static qsdp_status dequant_items(const qsdp_ditem* items, int32_t nitems, const 
     s.out = it.out;
     jobs.push_back(s);
   }
-  return run_dequant(jobs, cfg, acc, divisor, out_dtype, reinterpret_cast<cudaStream_t>(stream));
+  return run_dequant(jobs, cfg, acc, divisor, out_dtype, reinterpret_cast<cudaStream_t>(stream), DynSrc(), levels);
+}
+
+qsdp_status qsdp_dequantize_levels_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
+                                         const double* d_levels, int32_t nlevels, int32_t out_dtype,
+                                         void* stream) {
+  if (d_levels == nullptr) return fail(QSDP_EINVAL, "mode 'levels' requires a LevelTable");
+  if (cfg != nullptr && (cfg->bits < 1 || cfg->bits > 16 || nlevels != (1 << cfg->bits)))
+    return fail(QSDP_EINVAL, "level table size does not match bit_width");
+  return dequant_items(items, nitems, cfg, 0, 1, out_dtype, stream, d_levels);
+}
+
+qsdp_status qsdp_dequantize_levels(const uint8_t* codes, const float* meta, int64_t length,
+                                   const qsdp_qcfg* cfg, const double* d_levels, int32_t nlevels, void* out,
+                                   int32_t out_dtype, void* stream) {
+  qsdp_ditem it;
+  memset(&it, 0, sizeof(it));
+  it.codes[0] = codes;
+  it.meta[0] = meta;
+  it.nsrc = 1;
+  it.length = length;
+  it.out = out;
+  return qsdp_dequantize_levels_batch(&it, 1, cfg, d_levels, nlevels, out_dtype, stream);
+}
+
+qsdp_status qsdp_learn_levels(const double* d_values, int64_t n, double* d_levels, int32_t nlevels,
+                              double learning_rate, void* stream) {
+  if (nlevels < 1 || nlevels > 4096 || (nlevels & (nlevels - 1)) != 0)
+    return fail(QSDP_EINVAL, "level count must be a power of two <= 4096");
+  if (n < 1) return fail(QSDP_EINVAL, "cannot learn levels from an empty value set");
+  if (d_values == nullptr || d_levels == nullptr) return fail(QSDP_EINVAL, "null buffer");
+  cudaError_t e = launch_learn_levels(d_values, n, d_levels, nlevels, learning_rate,
+                                      reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "learn_levels kernel launch");
+  return QSDP_OK;
 }
 
 qsdp_status qsdp_dequantize_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,

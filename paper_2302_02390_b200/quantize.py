@@ -5,7 +5,8 @@ Reference interface mirrored here (pkg/src/qsdp/quantize.py):
 
 * ``quantize_bucket(values, bit_width, inner, rng)``       quantize.py:235-286
 * ``bucketed_quantize(v, bucket, bit_width, inner, rng)``  quantize.py:289-313
-* ``dequantize(block, mode)``                              quantize.py:209-232
+* ``dequantize(block, mode, levels)``                      quantize.py:209-232
+* inner mode ``"levels"`` (learned tables) routes to :mod:`.levels`
 * ``QuantizedBlock`` / ``BucketSpec``                      quantize.py:64-127
 * ``bucket_rng(root_seed, step, layer_idx, phase, worker, start)``
   (pkg/src/qsdp/sharded.py:235-240) returns a *key* the device generator
@@ -37,7 +38,7 @@ __all__ = [
 AFFINE_MODES = ("shift", "flip", "uniform_stochastic")
 INNER_MODES = AFFINE_MODES + ("levels",)
 _INNER_CODE = {"shift": _lib.INNER_SHIFT, "flip": _lib.INNER_STOCHASTIC,
-               "uniform_stochastic": _lib.INNER_STOCHASTIC}
+               "uniform_stochastic": _lib.INNER_STOCHASTIC, "levels": _lib.INNER_LEVELS}
 _DTYPE_CODE = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16}
 
 
@@ -55,8 +56,6 @@ class QuantSpec:
         if self.bucket < 1:
             raise ValueError(f"bucket_size must be >= 1, got {self.bucket}")
         if self.inner not in _INNER_CODE:
-            if self.inner == "levels":
-                raise NotImplementedError("learned levels are the next row (SURVEY §8(f) #1)")
             raise ValueError(f"unknown inner mode {self.inner!r}")
 
     def cfg(self) -> _lib.QCfg:
@@ -342,8 +341,8 @@ def quantize_bucket(values, bit_width: int, inner: str, rng: KeyedBucketRNG, lev
         raise ValueError("cannot quantize an empty bucket")
     if inner not in INNER_MODES:
         raise ValueError(f"unknown inner mode {inner!r}")
-    if levels is not None or inner == "levels":
-        raise NotImplementedError("learned levels are the next row (SURVEY §8(f) #1)")
+    if inner == "levels":  # no draws: rng is not consulted (quantize.py:275-279)
+        return _levels_blocks(v, v.size, bit_width, levels)[0]
     if not isinstance(rng, KeyedBucketRNG):
         raise TypeError("rng must come from bucket_rng(...): the device reproduces keyed streams")
     spec = QuantSpec(bit_width, v.size, inner)
@@ -365,8 +364,8 @@ def bucketed_quantize(v, bucket: BucketSpec, bit_width: int, inner: str = "shift
         raise ValueError("cannot quantize an empty vector")
     if not 1 <= bit_width <= 16:
         raise ValueError(f"bit_width must be in [1, 16], got {bit_width}")
-    if levels is not None:
-        raise NotImplementedError("learned levels are the next row (SURVEY §8(f) #1)")
+    if inner == "levels":
+        return _levels_blocks(v, bucket.bucket_size, bit_width, levels)
     if not isinstance(rng, KeyedBucketRNG):
         raise TypeError("rng must come from bucket_rng(...)")
     spec = QuantSpec(bit_width, bucket.bucket_size, inner)
@@ -383,13 +382,35 @@ def dequantize(block: QuantizedBlock, mode: str = "shift", levels=None) -> np.nd
     if codes.size and int(codes.max()) >= (1 << block.bit_width):
         raise ValueError(f"corrupted code >= 2**{block.bit_width} cannot be decoded")
     if mode == "levels":
-        raise NotImplementedError("learned levels are the next row (SURVEY §8(f) #1)")
+        if levels is None:
+            raise ValueError("mode 'levels' requires a LevelTable")
+        if levels.levels.size != (1 << block.bit_width):
+            raise ValueError("level table size does not match bit_width")
     dev = _device()
-    spec = QuantSpec(block.bit_width, block.length, "shift")
+    spec = QuantSpec(block.bit_width, block.length, "levels" if mode == "levels" else "shift")
     packed = torch.from_numpy(_pack(codes, block.bit_width)).to(dev)
     meta = torch.tensor([[block.shift, block.scale_lo, block.scale_hi]], dtype=torch.float32, device=dev)
     if float(np.float32(block.shift)) != block.shift or float(np.float32(block.scale_lo)) != block.scale_lo \
             or float(np.float32(block.scale_hi)) != block.scale_hi:
         raise ValueError("device dequantize takes float32-exact block metadata (the wire format's)")
-    out = dequantize_segment(packed, meta, block.length, spec, dtype=torch.float64)
+    if mode == "levels":
+        from .levels import dequantize_levels
+        out = dequantize_levels(packed, meta, block.length, spec, levels, dtype=torch.float64)
+    else:
+        out = dequantize_segment(packed, meta, block.length, spec, dtype=torch.float64)
     return out.cpu().numpy()
+
+
+def _levels_blocks(v: np.ndarray, bucket: int, bit_width: int, levels) -> list:
+    """inner="levels" over consecutive buckets on the GPU (quantize.py:275-279, 400-416)."""
+    if levels is None:
+        raise ValueError("inner 'levels' requires a LevelTable")
+    from .levels import quantize_levels
+    if not 1 <= bit_width <= 16:
+        raise ValueError(f"bit_width must be in [1, 16], got {bit_width}")
+    if levels.levels.size > (1 << bit_width):
+        raise ValueError(f"code out of range for bit_width {bit_width}")
+    spec = QuantSpec(bit_width, bucket, "levels")
+    x = torch.from_numpy(np.ascontiguousarray(v)).to(_device())
+    codes, meta = quantize_levels(x, spec, levels, check_finite=True)
+    return _blocks_from_device(codes, meta, v.size, bucket, bit_width)

@@ -72,3 +72,16 @@ def golden_hooks(g):
         yield dict(h=h, run=run, kind="ag" if kind == 0 else "rs", step=step, layer=layer, phase=phase,
                    P=P, wbits=wb, gbits=gb, bucket=S, seed=seed,
                    inp=g[f"hook_{h}_in"], out=g[f"hook_{h}_out"])
+
+
+def golden_level_cases(g):
+    """Yield the inner="levels" golden cases (quantize.py:225-286, 400-422)."""
+    for k, (ti, bits, S, n) in enumerate(g["lv_cases"]):
+        yield dict(k=k, table=g[f"lvtab_{int(ti)}"], bits=int(bits), bucket=int(S), n=int(n),
+                   x=g[f"lv_{k}_x"], codes=g[f"lv_{k}_codes"], meta=g[f"lv_{k}_meta"], deq=g[f"lv_{k}_deq"])
+
+
+def golden_learn_cases(g):
+    """Yield the learn_levels golden cases (quantize.py:366-397)."""
+    for k, lr in enumerate(g["ll_lr"]):
+        yield dict(k=k, lr=float(lr), values=g[f"ll_{k}_values"], init=g[f"ll_{k}_init"], out=g[f"ll_{k}_out"])

@@ -10,6 +10,11 @@ reference functions:
 * quant_*:  _segment_blocks(...) -> QuantizedBlock codes/scales/shift, encode()
             wire bytes, dequantize() fp64 (quantize.py:209-286, wire.py:108-131,
             sharded.py:243-248);
+* lv_*:     inner="levels" (quantize.py:235-286, 400-422) codes/scales and
+            dequantize(block, "levels", table) (quantize.py:225-231) over
+            uniform, learned, out-of-[0,1] and 2^12 / 2^16-level tables;
+* ll_*:     learn_levels(values, table, lr) outputs (quantize.py:366-397),
+            including the re-sort / collision-nudge and distinct-count paths;
 * hook_*:   inputs/outputs of ShardedMLP._gather / ._reduce_scatter recorded
             during a short ShardedMLP run (sharded.py:323-433), plus the run's
             ledger bits and losses, and ReferenceMLP's final parameters.
@@ -25,7 +30,7 @@ import sys
 
 import numpy as np
 
-from qsdp.quantize import dequantize
+from qsdp.quantize import BucketSpec, LevelTable, bucketed_quantize, dequantize, learn_levels
 from qsdp.sharded import (
     PHASE_GRAD,
     QuantConfig,
@@ -85,6 +90,72 @@ def _input(n, dtype, dist, rng):
     if dtype == "f32":
         x = x.astype(np.float32).astype(np.float64)
     return x
+
+
+def _level_tables(rng):
+    """(name, levels) tables for the levels-mode cases."""
+    tabs = [LevelTable.uniform(b).levels for b in (1, 2, 3, 4, 8)]
+    g = rng.standard_normal(20000)
+    g = (g - g.min()) / (g.max() - g.min())
+    for b, lr, passes in ((2, 0.01, 1), (3, 0.05, 2), (4, 0.01, 1), (8, 0.01, 1)):
+        t = LevelTable.uniform(b)
+        for _ in range(passes):
+            t = learn_levels(g, t, lr)
+        tabs.append(t.levels)
+    tabs.append(np.array([-0.5, 0.1, 0.2, 1.7]))                       # levels outside [0, 1]
+    tabs.append(np.array([0.0, 0.5, np.nextafter(0.5, 1.0), 1.0]))      # mid rounds onto a level
+    tabs.append(np.sort(rng.uniform(0, 1, 1 << 12)))                    # smem-staged widest
+    tabs.append(np.linspace(0.0, 1.0, 1 << 16) + rng.uniform(-1e-7, 1e-7, 1 << 16))  # global mids
+    return tabs
+
+
+def _levels(out):
+    rng = np.random.default_rng(402)
+    tabs = _level_tables(rng)
+    rows = []
+    for i, q in enumerate(tabs):
+        table = LevelTable(q)
+        bits = table.bit_width
+        out[f"lvtab_{i}"] = table.levels
+        for j, (S, n, dist, dtype) in enumerate([(1024, 3000, "normal", "f32"), (100, 333, "normal", "f64"),
+                                                 (7, 50, "ties", "f64"), (64, 640, "mids", "f64")]):
+            if dist == "mids":   # values landing exactly on the table's mids (lo=0, hi=1 buckets)
+                mids = (table.levels[:-1] + table.levels[1:]) / 2
+                x = np.resize(np.concatenate([[0.0, 1.0], np.clip(mids, 0, 1),
+                                              np.nextafter(np.clip(mids, 0, 1), 2)]), n)
+                for b0 in range(0, n, S):
+                    x[b0], x[b0 + 1] = 0.0, 1.0
+            else:
+                x = _input(n, dtype, dist, rng)
+            blocks = bucketed_quantize(x, BucketSpec(S), bits, "levels", levels=table)
+            k = len(rows)
+            out[f"lv_{k}_x"] = x.astype(np.float32) if dtype == "f32" else x
+            out[f"lv_{k}_codes"] = np.frombuffer(b"".join(_pack_codes(b.codes, bits) for b in blocks),
+                                                 dtype=np.uint8)
+            out[f"lv_{k}_meta"] = np.array([[b.shift, b.scale_lo, b.scale_hi] for b in blocks],
+                                           dtype=np.float32)
+            out[f"lv_{k}_deq"] = np.concatenate([dequantize(b, "levels", table) for b in blocks])
+            rows.append([i, bits, S, n])
+    out["lv_cases"] = np.array(rows, dtype=np.int64)
+    # learn_levels
+    lrows = []
+    g = rng.standard_normal(50000)
+    g = (g - g.min()) / (g.max() - g.min())
+    lcases = [(g[:5000], LevelTable.uniform(2).levels, 0.01), (g, LevelTable.uniform(4).levels, 0.01),
+              (g[:20000], LevelTable.uniform(8).levels, 0.05), (rng.uniform(0, 1, 3000), LevelTable.uniform(3).levels, 0.2),
+              (np.array([0.375, 0.9, 0.95, 0.99]), np.array([0.0, 0.25, 0.5, 1.0]), 2.0),   # collision -> nudge
+              (np.array([0.404, 0.1, 0.7, 0.2]), np.array([0.0, 0.4, 0.41, 1.0]), 3.0),    # crossing -> re-sort
+              (np.array([0.3, 0.3, 0.6]), LevelTable.uniform(2).levels, 0.1)]              # too few distinct
+    import warnings
+    for k, (v, q0, lr) in enumerate(lcases):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            res = learn_levels(v, LevelTable(q0), lr).levels
+        out[f"ll_{k}_values"] = np.asarray(v, dtype=np.float64)
+        out[f"ll_{k}_init"] = np.asarray(q0, dtype=np.float64)
+        out[f"ll_{k}_out"] = res
+        lrows.append(lr)
+    out["ll_lr"] = np.array(lrows)
 
 
 def main():
@@ -178,6 +249,7 @@ def main():
             out[f"run_{run_id}_param_{name}"] = v
         hook_rows.append(run_id)
     out["n_hooks"] = np.array(hook_idx)
+    _levels(out)
     out["n_runs"] = np.array(len(hook_rows))
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {os.path.getsize(OUT)/1e6:.2f} MB, {len(cases)} quant cases, "

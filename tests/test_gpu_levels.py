@@ -1,0 +1,211 @@
+"""Learned levels on the GPU vs golden vectors and the oracle.
+
+Bit-exact bar: codes, scales and fp64 dequantized values equal the reference's
+(quantize.py:225-286, 400-422); learn_levels tables equal the reference's
+sequential pass exactly (quantize.py:366-397).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_learn_cases, golden_level_cases
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2302_02390_b200 import levels
+    return levels
+
+
+def _q(L, x, bits, bucket, table, dt):
+    from paper_2302_02390_b200.quantize import QuantSpec
+    spec = QuantSpec(bits, bucket, "levels")
+    xt = torch.from_numpy(np.ascontiguousarray(x)).to(device="cuda", dtype=dt)
+    codes, meta = L.quantize_levels(xt, spec, table, check_finite=True)
+    return spec, codes, meta
+
+
+def test_levels_golden(golden, L):
+    cases = list(golden_level_cases(golden))
+    assert len(cases) >= 40
+    for c in cases:
+        table = L.LevelTable(c["table"])
+        dt = torch.float32 if c["x"].dtype == np.float32 else torch.float64
+        spec, codes, meta = _q(L, c["x"], c["bits"], c["bucket"], table, dt)
+        np.testing.assert_array_equal(codes.cpu().numpy(), c["codes"], err_msg=f"levels case {c['k']}")
+        np.testing.assert_array_equal(meta.cpu().numpy(), c["meta"], err_msg=f"levels case {c['k']}")
+        d64 = L.dequantize_levels(codes, meta, c["n"], spec, table, dtype=torch.float64)
+        np.testing.assert_array_equal(d64.cpu().numpy(), c["deq"], err_msg=f"levels case {c['k']}")
+        d32 = L.dequantize_levels(codes, meta, c["n"], spec, table, dtype=torch.float32)
+        np.testing.assert_array_equal(d32.cpu().numpy(), c["deq"].astype(np.float32))
+
+
+def test_learn_levels_golden(golden, L):
+    for c in golden_learn_cases(golden):
+        with pytest.warns(RuntimeWarning) if np.unique(c["values"]).size < c["init"].size else _null():
+            out = L.learn_levels(c["values"], L.LevelTable(c["init"]), c["lr"])
+        np.testing.assert_array_equal(out.levels, c["out"], err_msg=f"learn case {c['k']}")
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def test_levels_random_vs_oracle(oracle, L):
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        bits = int(rng.choice([1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 13, 16]))
+        nl = 1 << bits
+        kind = trial % 3
+        if kind == 0:
+            q = np.sort(rng.uniform(-0.2, 1.2, nl))
+        elif kind == 1:
+            q = np.linspace(0.0, 1.0, nl)
+        else:
+            q = np.cumsum(rng.exponential(1.0, nl))
+            q = (q - q[0]) / (q[-1] - q[0])
+        if np.any(np.diff(q) <= 0):
+            continue
+        table = L.LevelTable(q)
+        S = int(rng.choice([7, 64, 100, 256, 1024, 4096]))
+        n = int(rng.integers(1, 6 * S))
+        x = rng.standard_normal(n) * float(rng.choice([1e-3, 1.0, 1e6]))
+        if trial % 4 == 0:  # adversarial: values placed on the mids of lo=0/hi=1 buckets
+            mids = np.clip((q[:-1] + q[1:]) / 2, 0, 1)
+            x = np.resize(np.concatenate([[0.0, 1.0], mids, np.nextafter(mids, -1.0)]), n)
+            x[::S] = 0.0
+            x[1::S] = 1.0
+        f32 = trial % 2 == 1
+        if f32:
+            x = x.astype(np.float32)
+        spec, codes, meta = _q(L, x, bits, S, table, torch.float32 if f32 else torch.float64)
+        oc, om, bad = oracle.quantize_levels_segment(x.astype(np.float64), S, bits, q)
+        assert bad == -1
+        np.testing.assert_array_equal(codes.cpu().numpy(), oc, err_msg=f"trial {trial} bits {bits} S {S}")
+        np.testing.assert_array_equal(meta.cpu().numpy(), om)
+        d = L.dequantize_levels(codes, meta, n, spec, table).cpu().numpy()
+        np.testing.assert_array_equal(d, oracle.dequantize_levels_segment(oc, om, n, S, bits, q))
+
+
+def test_small_table_and_single_level(oracle, L):
+    # a 4-level table with 6-bit codes; a single-level table (all codes 0)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(500)
+    for q in (np.array([0.0, 0.1, 0.5, 1.0]), np.array([0.4])):
+        table = L.LevelTable(q)
+        _, codes, meta = _q(L, x, 6, 64, table, torch.float64)
+        oc, om, _ = oracle.quantize_levels_segment(x, 64, 6, _pad_table(q, 6))
+        np.testing.assert_array_equal(codes.cpu().numpy(), oc)
+        np.testing.assert_array_equal(meta.cpu().numpy(), om)
+
+
+def _pad_table(q, bits):
+    """The oracle takes a 2^bits table; codes of a smaller table equal those of
+    the same table padded with levels beyond every value (never selected)."""
+    pad = q[-1] + 1e6 * np.arange(1, (1 << bits) - q.size + 1)
+    return np.concatenate([q, pad])
+
+
+def test_reference_api_levels(L):
+    """quantize.py-mirroring API with inner="levels" (reference test_quantize.py:203-215, 267-273)."""
+    from paper_2302_02390_b200.quantize import BucketSpec, QuantizedBlock, bucketed_quantize, dequantize, \
+        quantize_bucket
+    block = QuantizedBlock(np.array([0, 1], dtype=np.uint32), 0.0, 0.0, 2.0, 1, 2)
+    with pytest.raises(ValueError):
+        dequantize(block, "levels")
+    assert np.allclose(dequantize(block, "levels", L.LevelTable(np.array([0.0, 1.0]))), [0.0, 2.0])
+    with pytest.raises(ValueError, match="does not match"):
+        dequantize(block, "levels", L.LevelTable.uniform(2))
+    rng = np.random.default_rng(38)
+    v = rng.standard_normal(600)
+    table = L.LevelTable.uniform(4)
+    blocks = bucketed_quantize(v, BucketSpec(), 4, "levels", None, levels=table)
+    out = np.concatenate([dequantize(b, "levels", table) for b in blocks])
+    span = blocks[0].scale_hi - blocks[0].scale_lo
+    assert np.abs(out - v).max() <= np.diff(table.levels).max() * span
+    assert all(b.shift == 0.0 for b in blocks)
+    with pytest.raises(ValueError):
+        quantize_bucket(v[:10], 4, "levels", None)
+    with pytest.raises(ValueError, match="non-finite"):
+        quantize_bucket(np.array([0.0, np.nan]), 4, "levels", None, levels=table)
+    b1 = quantize_bucket(v[:100], 4, "levels", None, levels=table)
+    assert b1 == bucketed_quantize(v[:100], BucketSpec(100), 4, "levels", levels=table)[0]
+
+
+def test_quantize_with_levels_kat(L):
+    t = L.LevelTable(np.array([0.0, 0.2, 0.7, 1.0]))
+    assert list(L.quantize_with_levels(np.array([0.0, 0.2, 0.7, 1.0]), t)) == [0, 1, 2, 3]
+    u = L.LevelTable.uniform(2)
+    mids = (u.levels[:-1] + u.levels[1:]) / 2
+    assert list(L.quantize_with_levels(mids, u)) == [0, 1, 2]
+    assert list(L.quantize_with_levels(np.array([-5.0, 5.0]), u)) == [0, 3]
+    assert list(L.quantize_with_levels(np.array([0.3, 0.9]), L.LevelTable(np.array([0.4])))) == [0, 0]
+
+
+def test_learn_levels_reference_behaviour(L):
+    """reference test_quantize.py:336-390 restated on the GPU path."""
+    t = L.LevelTable.uniform(2)
+    out = L.learn_levels(np.array([0.0, 1 / 3, 2 / 3, 1.0, 0.0]), t)
+    assert np.allclose(out.levels, t.levels)
+    out = L.learn_levels(np.array([0.2, 0.9]), L.LevelTable(np.array([0.0, 1.0])), learning_rate=0.01)
+    assert out.levels[0] == 0.0 - 0.01 * (0.0 - 0.2)
+    assert out.levels[1] == 1.0 - 0.01 * (1.0 - 0.9)
+    with pytest.warns(RuntimeWarning):
+        out = L.learn_levels(np.array([0.5, 0.5, 0.5]), L.LevelTable.uniform(3))
+    assert np.array_equal(out.levels, L.LevelTable.uniform(3).levels)
+    rng = np.random.default_rng(51)
+    out = L.learn_levels(rng.normal(0.5, 0.15, 5000).clip(0, 1), L.LevelTable.uniform(4))
+    assert np.all(np.diff(out.levels) > 0) and out.levels.size == 16
+    with pytest.raises(ValueError):
+        L.learn_levels(np.array([]), L.LevelTable.uniform(2))
+    with pytest.raises(ValueError, match="non-finite"):
+        L.learn_levels(np.array([0.1, np.inf, 0.3, 0.4]), L.LevelTable.uniform(1))
+
+
+def test_learn_levels_random_vs_oracle(oracle, L):
+    rng = np.random.default_rng(9)
+    for trial in range(6):
+        bits = int(rng.integers(0, 9))
+        v = rng.standard_normal(int(rng.integers(100, 20000)))
+        v = (v - v.min()) / (v.max() - v.min())
+        q0 = np.linspace(0.0, 1.0, 1 << bits) if bits else np.array([0.4])
+        lr = float(rng.choice([0.001, 0.01, 0.1, 0.7]))
+        out = L.learn_levels(v, L.LevelTable(q0), lr)
+        np.testing.assert_array_equal(out.levels, oracle.learn_levels(v, q0, lr))
+
+
+def test_learned_vs_uniform_error(oracle, L):
+    """experiments.py:405-441 and acceptance criterion 10 (test_acceptance.py:381-391)."""
+    rng = np.random.default_rng(2024_10)
+    values = rng.standard_normal(10 ** 5)
+    ue, le, table = L.learned_vs_uniform_error(values, bit_width=4)
+    assert 1 - le / ue >= 0.05
+    # restated on the host with the oracle's learn pass
+    S = 1024
+    norm = np.empty_like(values)
+    spans = []
+    for s in range(0, values.size, S):
+        seg = values[s:s + S]
+        lo, hi = seg.min(), seg.max()
+        spans.append((s, seg.size, lo, hi))
+        norm[s:s + seg.size] = (seg - lo) / (hi - lo) if hi > lo else 0.0
+    q = oracle.learn_levels(norm, np.linspace(0.0, 1.0, 16), 0.01)
+    np.testing.assert_array_equal(table.levels, q)
+
+    def rel(tab):
+        err = 0.0
+        for s, size, lo, hi in spans:
+            u = norm[s:s + size]
+            recon = lo + tab[oracle.level_codes(u, tab)] * (hi - lo)
+            err += float(((values[s:s + size] - recon) ** 2).sum())
+        return np.sqrt(err) / np.sqrt(float((values ** 2).sum()))
+
+    assert ue == pytest.approx(rel(np.linspace(0.0, 1.0, 16)), rel=1e-12)
+    assert le == pytest.approx(rel(q), rel=1e-12)

@@ -144,3 +144,59 @@ def test_oracle_mlp_matches_golden_run(golden):
             rs.append(e.reducescatter_bits)
         assert np.allclose(losses, golden[f"run_{run}_losses"], rtol=1e-12, atol=0)
         assert ag == list(golden[f"run_{run}_bits"][0]) and rs == list(golden[f"run_{run}_bits"][1])
+
+
+# -- learned levels -------------------------------------------
+
+
+def test_levels_quantizer_golden(golden, oracle):
+    from conftest import golden_level_cases
+    n = 0
+    for c in golden_level_cases(golden):
+        codes, meta, bad = oracle.quantize_levels_segment(c["x"].astype(np.float64), c["bucket"], c["bits"],
+                                                          c["table"])
+        assert bad == -1
+        np.testing.assert_array_equal(codes, c["codes"], err_msg=f"levels case {c['k']}")
+        np.testing.assert_array_equal(meta, c["meta"])
+        deq = oracle.dequantize_levels_segment(codes, meta, c["n"], c["bucket"], c["bits"], c["table"])
+        np.testing.assert_array_equal(deq, c["deq"])
+        n += 1
+    assert n >= 40
+
+
+def test_learn_levels_golden(golden, oracle):
+    from conftest import golden_learn_cases
+    for c in golden_learn_cases(golden):
+        out = oracle.learn_levels(c["values"], c["init"], c["lr"])
+        np.testing.assert_array_equal(out, c["out"], err_msg=f"learn case {c['k']}")
+
+
+def test_kat_quantize_with_levels(oracle):
+    # reference test_quantize.py: quantize_with_levels([0, .2, .7, 1], uniform(2)) == [0, 1, 2, 3]
+    q = np.linspace(0.0, 1.0, 4)
+    np.testing.assert_array_equal(oracle.level_codes([0.0, 0.2, 0.7, 1.0], q), [0, 1, 2, 3])
+    # searchsorted side="left": a value exactly on a mid takes the lower level
+    mids = (q[:-1] + q[1:]) / 2
+    np.testing.assert_array_equal(oracle.level_codes(mids, q), [0, 1, 2])
+    np.testing.assert_array_equal(oracle.level_codes(np.nextafter(mids, 2.0), q), [1, 2, 3])
+    # out-of-span values clamp to the end levels
+    np.testing.assert_array_equal(oracle.level_codes([-3.0, 7.0], q), [0, 3])
+
+
+@pytest.mark.reference
+def test_levels_live_reference_random(oracle, reference):
+    from qsdp.quantize import BucketSpec, LevelTable, bucketed_quantize, learn_levels
+    from qsdp.wire import _pack_codes
+    rng = np.random.default_rng(5)
+    for trial in range(6):
+        bits = int(rng.integers(1, 7))
+        g = rng.standard_normal(4000)
+        g = (g - g.min()) / (g.max() - g.min())
+        lr = float(rng.uniform(0.001, 0.1))
+        table = learn_levels(g, LevelTable.uniform(bits), lr)
+        np.testing.assert_array_equal(oracle.learn_levels(g, LevelTable.uniform(bits).levels, lr), table.levels)
+        S = int(rng.integers(5, 300))
+        x = rng.standard_normal(int(rng.integers(1, 2000)))
+        blocks = bucketed_quantize(x, BucketSpec(S), bits, "levels", levels=table)
+        codes, meta, _ = oracle.quantize_levels_segment(x, S, bits, table.levels)
+        assert codes.tobytes() == b"".join(_pack_codes(b.codes, bits) for b in blocks)
