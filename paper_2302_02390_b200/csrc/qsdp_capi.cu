@@ -35,9 +35,9 @@ cudaError_t upload_jump_f32(const JumpEntry* host);
 cudaError_t upload_jump_f64(const JumpEntry* host);
 cudaError_t upload_jump_fused(const JumpEntry* host);
 cudaError_t launch_fused(const QJobTable& qt, const DJobTable& dt, const FuseSync& fs, int sms, cudaStream_t s);
-cudaError_t launch_quantize_levels(const QJobTable& tab, int in_f64, const double* levels, int nl, int sms,
+cudaError_t launch_quantize_levels(const QJobTable& tab, int in_f64, const double* levels, int nl, bool vec, int sms,
                                    cudaStream_t s);
-cudaError_t launch_dequant_levels(const DJobTable& tab, const double* levels, int sms, cudaStream_t s);
+cudaError_t launch_dequant_levels(const DJobTable& tab, const double* levels, bool vec, int sms, cudaStream_t s);
 cudaError_t launch_learn_levels(const double* values, int64_t n, double* q, int nl, double lr, cudaStream_t s);
 }  // namespace qsdp
 
@@ -178,7 +178,9 @@ qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const q
     bool vec = false;
     build_qtab(tab, jobs, i, cfg, d_bad, dyn, vec);
     if (tab.njobs == 0) continue;
-    cudaError_t e = levels != nullptr      ? launch_quantize_levels(tab, x_dtype == QSDP_F64, levels, nlevels, sms, stream)
+    bool codes_ok = true;  // wide code stores of the levels fast path
+    for (int k = 0; k < tab.njobs; ++k) codes_ok = codes_ok && aligned(tab.jobs[k].codes, 8);
+    cudaError_t e = levels != nullptr      ? launch_quantize_levels(tab, x_dtype == QSDP_F64, levels, nlevels, vec && codes_ok, sms, stream)
                     : x_dtype == QSDP_F64 ? launch_quantize_f64(tab, vec, sms, stream)
                                           : launch_quantize_f32(tab, vec, sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "quantize kernel launch");
@@ -246,7 +248,9 @@ qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg,
     bool vec = false;
     build_dtab(tab, jobs, i, cfg, accumulate, divisor, out_dtype, dyn, vec);
     if (tab.njobs == 0) continue;
-    cudaError_t e = levels != nullptr ? launch_dequant_levels(tab, levels, sms, stream)
+    bool out16 = true;  // 16-byte vector stores of the levels fast path (bf16 included)
+    for (int k = 0; k < tab.njobs; ++k) out16 = out16 && aligned(tab.jobs[k].out, 16);
+    cudaError_t e = levels != nullptr ? launch_dequant_levels(tab, levels, vec && out16 && tab.codes_vec, sms, stream)
                                       : launch_dequant(tab, vec, sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "dequantize kernel launch");
   }

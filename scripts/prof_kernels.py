@@ -20,6 +20,7 @@ ap.add_argument("--reps", type=int, default=11)
 ap.add_argument("--bits", type=int, default=8)
 ap.add_argument("--gbits", type=int, default=8)
 ap.add_argument("--bucket", type=int, default=1024)
+ap.add_argument("--levels", action="store_true", help="also time the levels-mode kernels (LQ/LD) and learn_levels")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 n = a.n
@@ -39,6 +40,23 @@ kern = {
     "K2": (lambda s: quantize_segments([(g, 0, SegmentKey(0, s, 0, 2, 0))], gs, out=[gq]), 4 * n + cbg),
     "K4": (lambda s: dequant_accumulate([gq], n, gs, 1, out=out), cbg + 4 * n),
 }
+if a.levels:
+    from paper_2302_02390_b200.levels import LevelTable, dequantize_levels, learn_levels, quantize_levels_segments
+    ls = QuantSpec(a.bits, a.bucket, "levels")
+    u = torch.rand(200000, device=dev, dtype=torch.float64)
+    table = learn_levels(u, LevelTable.uniform(a.bits))
+    lq = (torch.empty(codes_bytes(n, ls) + 16, dtype=torch.uint8, device=dev),
+          torch.empty((num_buckets(n, a.bucket), 3), device=dev))
+    cbl = codes_bytes(n, ls) + 12 * num_buckets(n, a.bucket)
+    kern["LQ"] = (lambda s: quantize_levels_segments([x], ls, table, out=[lq]), 4 * n + cbl)
+    kern["LD"] = (lambda s: dequantize_levels(lq[0], lq[1], n, ls, table, dtype=torch.float32, out=out), cbl + 4 * n)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    learn_levels(u, LevelTable.uniform(a.bits))
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"learn_levels: {u.numel()} values, {a.bits}-bit table: {e0.elapsed_time(e1):.2f} ms "
+          f"({u.numel() / e0.elapsed_time(e1) / 1e3:.2f} M values/s)")
 res = {k: 0.0 for k in kern}
 for r in range(a.reps):
     for k, (fn, nb) in kern.items():

@@ -60,7 +60,7 @@ class _null:
 
 def test_levels_random_vs_oracle(oracle, L):
     rng = np.random.default_rng(11)
-    for trial in range(40):
+    for trial in range(60):
         bits = int(rng.choice([1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 13, 16]))
         nl = 1 << bits
         kind = trial % 3
@@ -74,7 +74,7 @@ def test_levels_random_vs_oracle(oracle, L):
         if np.any(np.diff(q) <= 0):
             continue
         table = L.LevelTable(q)
-        S = int(rng.choice([7, 64, 100, 256, 1024, 4096]))
+        S = int(rng.choice([7, 64, 100, 256, 512, 1024, 2048, 4096]))
         n = int(rng.integers(1, 6 * S))
         x = rng.standard_normal(n) * float(rng.choice([1e-3, 1.0, 1e6]))
         if trial % 4 == 0:  # adversarial: values placed on the mids of lo=0/hi=1 buckets
@@ -92,6 +92,27 @@ def test_levels_random_vs_oracle(oracle, L):
         np.testing.assert_array_equal(meta.cpu().numpy(), om)
         d = L.dequantize_levels(codes, meta, n, spec, table).cpu().numpy()
         np.testing.assert_array_equal(d, oracle.dequantize_levels_segment(oc, om, n, S, bits, q))
+
+
+@pytest.mark.parametrize("kind", ["overflow_span", "subnormal_span", "tiny_span", "f64_wide"])
+def test_levels_extreme_ranges(oracle, L, kind):
+    """f32 spans that overflow / underflow the f32 prefilter (fp64 path) and tiny spans."""
+    rng = np.random.default_rng(17)
+    table = L.LevelTable(np.sort(rng.uniform(0, 1, 16)))
+    n, S = 4096, 1024
+    if kind == "overflow_span":
+        x = (rng.uniform(-1, 1, n) * 3.4e38).astype(np.float32)
+    elif kind == "subnormal_span":
+        x = (rng.integers(0, 50, n) * np.float32(1.4e-45)).astype(np.float32)
+    elif kind == "tiny_span":
+        x = (np.float32(1.0) + rng.integers(0, 9, n).astype(np.float32) * np.float32(2 ** -23)).astype(np.float32)
+    else:
+        x = rng.standard_normal(n) * 1e300
+    _, codes, meta = _q(L, x, 4, S, table, torch.float32 if x.dtype == np.float32 else torch.float64)
+    oc, om, bad = oracle.quantize_levels_segment(x.astype(np.float64), S, 4, table.levels)
+    assert bad == -1
+    np.testing.assert_array_equal(codes.cpu().numpy(), oc)
+    np.testing.assert_array_equal(meta.cpu().numpy(), om)
 
 
 def test_small_table_and_single_level(oracle, L):
