@@ -196,7 +196,7 @@ __device__ __forceinline__ int count_below(const double* mids, int nm, double t)
 struct LevelIndex {
   const double* mids;
   const double* cmid;    // fp64 index (f64 inputs)
-  const float* cmid32;   // fp32 prefilter index (f32 inputs), same smem
+  const float* cmid32;   // fp32 prefilter index (f32 inputs): float2 {cmid, base bits}, same smem
   const uint16_t* base;
   int nm;         // number of mids = nl - 1
   double ulo, uhi;  // clip(clip(u, 0, 1), q0, qL) == clip(u, ulo, uhi)
@@ -239,10 +239,10 @@ struct LevelIndex {
     float u = __fmul_rn(__fsub_rn(x, lof), inv32);
     u = fminf(fmaxf(u, ulo32), uhi32);
     const int t = __float_as_int(__fadd_rn(u, 3072.0f)) & 0x3FFFFF;  // round(u * 4096): ulp(3072) = 2^-12
-    const uint16_t b = base[t];
-    const float d = __fsub_rn(u, cmid32[t]);
-    slow = (b & kMulti) || fabsf(d) <= 1e-6f;
-    return (uint32_t)(b & 0x7fff) + (d > 0.0f ? 1u : 0u);
+    const float2 e = reinterpret_cast<const float2*>(cmid32)[t];     // {cmid (NaN: multi-mid cell), base}
+    const float d = __fsub_rn(u, e.x);
+    slow = !(fabsf(d) > 1e-6f);
+    return (uint32_t)__float_as_int(e.y) + (d > 0.0f ? 1u : 0u);
   }
 };
 
@@ -262,7 +262,8 @@ __device__ __forceinline__ LevelIndex level_index_view(double* sm, const double*
   return ix;
 }
 
-// smem: mids[nl] doubles, cmid[kCells + 1] doubles (or floats: F32), base[kCells + 1] uint16
+// smem: mids[nl] doubles, then cmid[kCells + 1] doubles + base[kCells + 1] uint16
+// (f64 inputs) or {cmid, base} float2 entries (F32: the prefilter index)
 template <bool F32>
 __device__ __forceinline__ LevelIndex build_level_index(double* sm, const double* levels, int nl) {
   double* cmid = sm + nl;
@@ -283,9 +284,13 @@ __device__ __forceinline__ LevelIndex build_level_index(double* sm, const double
       const double wlo = __dsub_rn(((double)c - 0.5) * h, margin), whi = __dadd_rn(((double)c + 0.5) * h, margin);
       while (plo < nm && sm[plo] < wlo) ++plo;  // plo = #{mids < wlo}
       while (phi < nm && sm[phi] < whi) ++phi;  // phi = #{mids < whi}
-      base[c] = (uint16_t)plo | (phi - plo >= 2 ? kMulti : 0);
-      if (F32) reinterpret_cast<float*>(cmid)[c] = phi - plo == 1 ? __double2float_rn(sm[plo]) : INFINITY;
-      else cmid[c] = phi - plo == 1 ? sm[plo] : INFINITY;
+      if (F32) {
+        const float cm = phi - plo == 1 ? __double2float_rn(sm[plo]) : (phi - plo == 0 ? INFINITY : __int_as_float(0x7fc00000));
+        reinterpret_cast<float2*>(cmid)[c] = make_float2(cm, __int_as_float(plo));
+      } else {
+        base[c] = (uint16_t)plo | (phi - plo >= 2 ? kMulti : 0);
+        cmid[c] = phi - plo == 1 ? sm[plo] : INFINITY;
+      }
     }
   }
   __syncthreads();
