@@ -196,6 +196,9 @@ qsdp_status qsdp_comm_set_step_source(qsdp_comm* c, const uint64_t* d_step);
 /* 1 (opt-in; env QSDP_FUSED=1 sets it at creation): run each collective as ONE persistent
  * kernel -- quantize, in-kernel grid + cross-GPU barrier, pull-dequantize -- when the
  * configuration allows (fp32 input, 2/4/8/16 bits, bucket 128..2048, aligned output). */
+/* Learned weight levels for the all-gather (w.inner == QSDP_INNER_LEVELS): a
+ * device float64[2^w.bits] table that stays valid while the comm uses it. */
+qsdp_status qsdp_comm_set_weight_levels(qsdp_comm* c, const double* d_levels, int32_t nlevels);
 qsdp_status qsdp_comm_set_fused(qsdp_comm* c, int32_t enable);
 /* Quantized all-gather (ShardedMLP._gather): this rank's shard = segs[rank];
  * every rank writes the dequantized full tensor (sum of segs lengths) to full_out.

@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "qsdp_all_gather", "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_batch_dstep",
     "qsdp_counter_add", "qsdp_comm_set_step_source", "qsdp_comm_set_fused",
     "qsdp_quantize_levels", "qsdp_quantize_levels_batch", "qsdp_dequantize_levels",
-    "qsdp_dequantize_levels_batch", "qsdp_learn_levels",
+    "qsdp_dequantize_levels_batch", "qsdp_learn_levels", "qsdp_comm_set_weight_levels",
 )
 
 
@@ -108,6 +108,7 @@ def lib():
     L.qsdp_counter_add.argtypes = [vp, ctypes.c_uint64, vp]
     L.qsdp_comm_set_step_source.argtypes = [vp, vp]
     L.qsdp_comm_set_fused.argtypes = [vp, i32]
+    L.qsdp_comm_set_weight_levels.argtypes = [vp, vp, i32]
     L.qsdp_dequantize.argtypes = [vp, vp, i64, cfgp, vp, i32, vp]
     L.qsdp_dequantize_batch.argtypes = [ctypes.POINTER(DItem), i32, cfgp, i32, vp]
     L.qsdp_dequant_accumulate.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i64, cfgp,
@@ -132,7 +133,7 @@ def lib():
                  "qsdp_comm_ipc_handle", "qsdp_comm_open_peers", "qsdp_all_gather",
                  "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_levels",
                  "qsdp_quantize_levels_batch", "qsdp_dequantize_levels", "qsdp_dequantize_levels_batch",
-                 "qsdp_learn_levels"):
+                 "qsdp_learn_levels", "qsdp_comm_set_weight_levels"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib

@@ -91,7 +91,8 @@ class QSDPComm:
     """NVLink peer-memory communicator for QSDP's quantized AG / RS."""
 
     def __init__(self, max_segment_elems: int, wspec: QuantSpec, gspec: QuantSpec,
-                 group: dist.ProcessGroup | None = None, device: torch.device | None = None):
+                 group: dist.ProcessGroup | None = None, device: torch.device | None = None,
+                 weight_levels=None):
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -118,6 +119,18 @@ class QSDPComm:
             cb = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
             _lib.check(L.qsdp_comm_open_peers(self._h, cb))
             dist.barrier(group=group)
+        if weight_levels is not None:
+            self.set_weight_levels(weight_levels)
+
+    def set_weight_levels(self, table) -> None:
+        """Learned weight levels: with ``wspec.inner == "levels"``
+        the all-gather quantizes / dequantizes through ``table`` (a
+        :class:`~.levels.LevelTable` of 2^bits levels, kept on this device)."""
+        if self.wspec.inner != "levels":
+            raise ValueError("weight spec is not inner='levels'")
+        q = table.device(self.device)
+        self._wlevels = q  # keep alive while the comm uses it
+        _lib.check(_lib.lib().qsdp_comm_set_weight_levels(self._h, q.data_ptr(), q.numel()))
 
     def set_step_source(self, counter: torch.Tensor | None) -> None:
         """Keys use ``key.step + counter`` read on the device (graph replay)."""

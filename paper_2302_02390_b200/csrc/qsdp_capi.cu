@@ -549,6 +549,8 @@ struct qsdp_comm {
   bool opened[QSDP_MAX_WORLD] = {};
   const unsigned long long* step_src = nullptr;
   bool fused = true;  // single-launch collectives when the configuration allows
+  const double* wlevels = nullptr;  // learned weight table (w.inner == QSDP_INNER_LEVELS)
+  int wnlevels = 0;
 
   static constexpr size_t kFlagBytes = 256;
   uint8_t* slot(uint8_t* b, int idx) const { return b + kFlagBytes + (size_t)idx * slot_bytes; }  // parity 0
@@ -573,7 +575,7 @@ qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32
   if (out == nullptr) return fail(QSDP_EINVAL, "null out");
   if (world < 1 || world > QSDP_MAX_WORLD || rank < 0 || rank >= world)
     return fail(QSDP_EINVAL, "world must be in [1, 8] and 0 <= rank < world");
-  qsdp_status st = check_cfg(wcfg);
+  qsdp_status st = check_cfg(wcfg, wcfg != nullptr && wcfg->inner == QSDP_INNER_LEVELS);
   if (st != QSDP_OK) return st;
   st = check_cfg(gcfg);
   if (st != QSDP_OK) return st;
@@ -613,6 +615,16 @@ qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32
   const char* env = getenv("QSDP_FUSED");
   c->fused = env != nullptr && env[0] == '1';
   *out = c;
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_comm_set_weight_levels(qsdp_comm* c, const double* d_levels, int32_t nlevels) {
+  if (c == nullptr) return fail(QSDP_EINVAL, "null comm");
+  if (c->w.inner != QSDP_INNER_LEVELS) return fail(QSDP_EINVAL, "weight config is not inner 'levels'");
+  if (d_levels == nullptr || nlevels != (1 << c->w.bits))
+    return fail(QSDP_EINVAL, "level table size does not match bit_width");
+  c->wlevels = d_levels;
+  c->wnlevels = nlevels;
   return QSDP_OK;
 }
 
@@ -721,7 +733,7 @@ static QJobSpec comm_qjob(const void* x, const qsdp_segment& seg, uint8_t* slot,
 // direct widths, buckets of 128..2048 elements, vector-aligned outputs.
 static bool fused_cfg_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
   const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
-  return c->fused && in_dtype == QSDP_F32 && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 128 &&
+  return c->fused && cfg->inner != QSDP_INNER_LEVELS && in_dtype == QSDP_F32 && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 128 &&
          cfg->bucket * 4 <= 8192;
 }
 
@@ -768,6 +780,8 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
   if (st != QSDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const qsdp_qcfg* cfg = &c->w;
+  const bool lv = cfg->inner == QSDP_INNER_LEVELS;
+  if (lv && c->wlevels == nullptr) return fail(QSDP_EINVAL, "inner 'levels' requires a LevelTable (qsdp_comm_set_weight_levels)");
   std::vector<QJobSpec> q(1, comm_qjob(shard, segs[c->rank], c->slot(c->base, 0), c->slot_codes, *key, 0));
   std::vector<DJobSpec> d(c->world);
   const size_t osz = dtype_size(out_dtype);
@@ -786,7 +800,7 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
     if (st != QSDP_OK || launched) return st;
   }
   // 1. quantize this rank's shard into its local slot (key worker 0, sharded.py:341)
-  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1), lv ? c->wlevels : nullptr, c->wnlevels);
   if (st != QSDP_OK) return st;
   // 2. publish + wait for every peer's slot of this call
   if (c->world > 1) {
@@ -794,7 +808,7 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
     if (st != QSDP_OK) return st;
   }
   // 3. pull-dequantize all P shards over NVLink into the gathered buffer
-  return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0));
+  return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0), lv ? c->wlevels : nullptr);
 }
 
 qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_dtype, const qsdp_segment* segs,

@@ -137,15 +137,16 @@ __global__ void __launch_bounds__(256) dequant_levels_kernel(const __grid_consta
   const int S = tab.bucket, bits = tab.bits;
   const uint32_t mask = (1u << bits) - 1u;
   const int64_t pbs = payload_bytes(S, bits);
+  const int64_t poff = d_parity_off(tab);  // communicator slot parity (0 outside collectives)
   for (int64_t b = warp; b < tab.total_buckets; b += nwarps) {
     const int j = find_job_d(tab, b);
     const DJob& J = tab.jobs[j];
     const int64_t lb = b - J.bucket_base, off = lb * S;
     const int n = (int)min((int64_t)S, J.length - off);
-    const float* m = J.meta[0] + 3 * lb;
+    const float* m = meta_at(J.meta[0], poff) + 3 * lb;
     const double lo = (double)m[1];
     const double span = __dsub_rn((double)m[2], lo);  // scale_hi - scale_lo
-    const uint8_t* cp = J.codes[0] + lb * pbs;
+    const uint8_t* cp = J.codes[0] + poff + lb * pbs;
     const int64_t lim = payload_bytes(n, bits);
     for (int e = lane; e < n; e += 32) {
       const int64_t bit = (int64_t)e * bits, by = bit >> 3;
@@ -517,15 +518,16 @@ __global__ void __launch_bounds__(256) dequant_levels_vec_kernel(const __grid_co
   const int S = tab.bucket, bits = tab.bits;
   const uint32_t mask = (1u << bits) - 1u;
   const int64_t pbs = payload_bytes(S, bits);
+  const int64_t poff = d_parity_off(tab);  // communicator slot parity (0 outside collectives)
   for (int64_t b = warp; b < tab.total_buckets; b += nwarps) {
     const int j = find_job_d(tab, b);
     const DJob& J = tab.jobs[j];
     const int64_t lb = b - J.bucket_base, off = lb * S;
     const int n = (int)min((int64_t)S, J.length - off);
-    const float* m = J.meta[0] + 3 * lb;
+    const float* m = meta_at(J.meta[0], poff) + 3 * lb;
     const double lo = (double)m[1];
     const double span = __dsub_rn((double)m[2], lo);
-    const uint8_t* cp = J.codes[0] + lb * pbs;
+    const uint8_t* cp = J.codes[0] + poff + lb * pbs;
     const int64_t lim = payload_bytes(n, bits);
     for (int o = lane; 8 * o < n; o += 32) {
       const uint8_t* p = cp + (int64_t)o * bits;

@@ -97,12 +97,40 @@ def main():
                 failures += 1
                 print(f"rank {rank} size {size} graph replay {rep}: mismatch", flush=True)
         comm.close()
+    failures += levels_all_gather(rank, world, dev)
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
     if rank == 0:
         print(f"dist_comm_check world={world}: {'OK' if t.item() == 0 else 'FAILED'}", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if t.item() == 0 else 1)
+
+
+def levels_all_gather(rank, world, dev):
+    """C1 with learned weight levels (SURVEY §8(f) #1) vs the oracle's levels codec."""
+    from paper_2302_02390_b200.levels import LevelTable
+    fails = 0
+    for size, bucket, wb in [(1 << 20, 1024, 5), (300001, 256, 6)]:
+        segs = plan_segments(size, world, 1)
+        g = np.random.default_rng(3).standard_normal(50000)
+        q = O.learn_levels((g - g.min()) / (g.max() - g.min()), np.linspace(0.0, 1.0, 1 << wb), 0.01)
+        comm = QSDPComm(max(n for _, n in segs), QuantSpec(wb, bucket, "levels"), QuantSpec(8, bucket, "uniform_stochastic"),
+                        weight_levels=LevelTable(q))
+        full = (np.random.default_rng(size).standard_normal(size) * 0.02).astype(np.float32)
+        s, n = segs[rank]
+        out = torch.empty(size, dtype=torch.float32, device=dev)
+        for step in range(2):
+            comm.all_gather(torch.from_numpy(full[s:s + n]).to(dev), segs, SegmentKey(0, step, 1, 0, 0), out)
+            exp = np.zeros(size)
+            for sq, nq in segs:
+                if nq:
+                    c, m, _ = O.quantize_levels_segment(full[sq:sq + nq], bucket, wb, q)
+                    exp[sq:sq + nq] = O.dequantize_levels_segment(c, m, nq, bucket, wb, q)
+            if not np.array_equal(out.cpu().numpy(), exp.astype(np.float32)):
+                fails += 1
+                print(f"rank {rank} levels size {size} step {step}: mismatch", flush=True)
+        comm.close()
+    return fails
 
 
 if __name__ == "__main__":

@@ -74,6 +74,25 @@ def test_graph_replay_with_device_step(oracle, fused):
     comm.close()
 
 
+def test_levels_all_gather_single_rank(oracle):
+    """C1 with learned weight levels; a missing table fails loudly."""
+    from paper_2302_02390_b200.levels import LevelTable
+    dev = torch.device("cuda", 0)
+    size, bucket, wb = 1024 * 77 + 5, 1024, 6
+    q = np.sort(np.random.default_rng(2).uniform(0, 1, 1 << wb))
+    comm = QSDPComm(size, QuantSpec(wb, bucket, "levels"), QuantSpec(8, bucket, "uniform_stochastic"), device=dev)
+    x = (np.random.default_rng(5).standard_normal(size) * 0.02).astype(np.float32)
+    out = torch.empty(size, device=dev)
+    with pytest.raises(ValueError, match="LevelTable"):
+        comm.all_gather(torch.from_numpy(x).to(dev), [(0, size)], SegmentKey(0, 0, 1, 0, 0), out)
+    comm.set_weight_levels(LevelTable(q))
+    comm.all_gather(torch.from_numpy(x).to(dev), [(0, size)], SegmentKey(0, 0, 1, 0, 0), out)
+    c, m, _ = oracle.quantize_levels_segment(x, bucket, wb, q)
+    exp = oracle.dequantize_levels_segment(c, m, size, bucket, wb, q).astype(np.float32)
+    assert np.array_equal(out.cpu().numpy(), exp)
+    comm.close()
+
+
 def test_plan_segments():
     assert plan_segments(10, 4) == [(0, 2), (2, 2), (4, 2), (6, 4)]
     assert plan_segments(10, 4, pad_to=4) == [(0, 4), (4, 4), (8, 2), (10, 0)]
