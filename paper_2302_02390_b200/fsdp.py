@@ -36,14 +36,17 @@ class QSDPContext:
     """Shared state of one QSDP training run: communicators, step and phase."""
 
     def __init__(self, max_shard_numel: int, wspec: QuantSpec, gspec: QuantSpec, root_seed: int = 0,
-                 group: dist.ProcessGroup | None = None, device: torch.device | None = None):
+                 group: dist.ProcessGroup | None = None, device: torch.device | None = None,
+                 weight_levels=None):
         self.wspec, self.gspec = wspec, gspec
         self.root_seed = root_seed
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         # FSDP2 issues all-gathers and reduce-scatters on different streams: one
         # communicator (slots + device epoch) per stream keeps each sequence ordered.
-        self.ag = QSDPComm(max_shard_numel, wspec, gspec, group=group, device=device)
+        # wspec.inner == "levels": the all-gather codes weights through a learned
+        # table (levels.LevelTable, e.g. levels.learn_weight_levels(model weights))
+        self.ag = QSDPComm(max_shard_numel, wspec, gspec, group=group, device=device, weight_levels=weight_levels)
         self.rs = QSDPComm(max_shard_numel, wspec, gspec, group=group, device=device)
         self.step = 0
         self.phase = PHASE_W_FWD

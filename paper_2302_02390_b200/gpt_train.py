@@ -45,8 +45,9 @@ def _shard_numel(params, world: int) -> int:
 
 
 def shard_model(model, mode: str, wspec: QuantSpec | None = None, gspec: QuantSpec | None = None,
-                root_seed: int = 0):
-    """fully_shard every transformer block and the root; install QSDP comms if mode == 'qsdp'."""
+                root_seed: int = 0, weight_levels=None):
+    """fully_shard every transformer block and the root; install QSDP comms if mode == 'qsdp'
+    (``weight_levels``: a LevelTable when ``wspec.inner == "levels"``)."""
     from torch.distributed.device_mesh import init_device_mesh
     from torch.distributed.fsdp import MixedPrecisionPolicy, fully_shard
 
@@ -66,7 +67,7 @@ def shard_model(model, mode: str, wspec: QuantSpec | None = None, gspec: QuantSp
         from .fsdp import QSDPContext, apply_qsdp
         ctx = QSDPContext(max_shard + 4096, wspec or QuantSpec(8, 1024, "shift"),
                           gspec or QuantSpec(8, 1024, "uniform_stochastic"), root_seed=root_seed,
-                          device=torch.device("cuda", torch.cuda.current_device()))
+                          device=torch.device("cuda", torch.cuda.current_device()), weight_levels=weight_levels)
         apply_qsdp(blocks + [model], ctx)
     return ctx
 

@@ -30,7 +30,7 @@ from . import _lib
 from .quantize import QuantSpec, _DTYPE_CODE, _require_cuda, _stream, codes_bytes, num_buckets
 
 __all__ = ["LevelTable", "learn_levels", "quantize_with_levels", "quantize_levels", "quantize_levels_segments",
-           "dequantize_levels", "learned_vs_uniform_error"]
+           "dequantize_levels", "learned_vs_uniform_error", "normalize_buckets", "learn_weight_levels"]
 
 
 class LevelTable:
@@ -212,22 +212,11 @@ def learned_vs_uniform_error(values, bit_width: int, bucket_size: int = 1024, pa
     reduced on the device (summation order differs from numpy's: ~1e-15 rel)."""
     x = _as_device_f64(values)
     n = x.numel()
-    nb = -(-n // bucket_size)
-    pad = nb * bucket_size - n
-    xp = torch.cat([x, x[-1:].expand(pad)]) if pad else x  # padding repeats a member: min/max unchanged
-    tiles = xp.view(nb, bucket_size)
-    lo = tiles.amin(dim=1, keepdim=True)
-    hi = tiles.amax(dim=1, keepdim=True)
-    span = hi - lo
-    norm = torch.where(span > 0, (tiles - lo) / torch.where(span > 0, span, torch.ones_like(span)),
-                       torch.zeros_like(tiles))
-    normalized = norm.reshape(-1)[:n].contiguous()
+    normalized, lo_e, span_e = normalize_buckets(x, bucket_size)
     table = LevelTable.uniform(bit_width)
     for _ in range(passes):
         table = learn_levels(normalized, table, learning_rate)
     uniform = LevelTable.uniform(bit_width)
-    lo_e = lo.expand(nb, bucket_size).reshape(-1)[:n]
-    span_e = span.expand(nb, bucket_size).reshape(-1)[:n]
 
     def rel_err(tab):
         q = tab.device(x.device)
@@ -235,3 +224,37 @@ def learned_vs_uniform_error(values, bit_width: int, bucket_size: int = 1024, pa
         return math.sqrt(float(((x - recon) ** 2).sum())) / math.sqrt(float((x * x).sum()))
 
     return rel_err(uniform), rel_err(table), table
+
+
+def normalize_buckets(x: torch.Tensor, bucket_size: int):
+    """Bucket-wise fp64 min-max normalisation as in experiments.py:418-426:
+    returns (u, lo, span) per element, u = (x - lo) / span (0 where span == 0)."""
+    x = x.reshape(-1).to(torch.float64)
+    n = x.numel()
+    nb = -(-n // bucket_size)
+    pad = nb * bucket_size - n
+    xp = torch.cat([x, x[-1:].expand(pad)]) if pad else x  # padding repeats a member: min/max unchanged
+    tiles = xp.view(nb, bucket_size)
+    lo = tiles.amin(dim=1, keepdim=True)
+    span = tiles.amax(dim=1, keepdim=True) - lo
+    u = torch.where(span > 0, (tiles - lo) / torch.where(span > 0, span, torch.ones_like(span)),
+                    torch.zeros_like(tiles))
+    lo_e = lo.expand(nb, bucket_size).reshape(-1)[:n]
+    span_e = span.expand(nb, bucket_size).reshape(-1)[:n]
+    return u.reshape(-1)[:n].contiguous(), lo_e, span_e
+
+
+def learn_weight_levels(tensors, bit_width: int, bucket_size: int = 1024, learning_rate: float = 0.01,
+                        passes: int = 1, max_values: int = 1 << 18, seed: int = 0) -> LevelTable:
+    """A weight level table for the levels all-gather: the bucket-normalised
+    values of ``tensors`` (a strided sample of at most ``max_values``), then
+    ``passes`` learn_levels passes from the uniform table (Alg. 2)."""
+    us = [normalize_buckets(t.detach().reshape(-1), bucket_size)[0] for t in tensors if t.numel()]
+    u = torch.cat(us)
+    if u.numel() > max_values:
+        g = torch.Generator(device=u.device).manual_seed(seed)
+        u = u[torch.randperm(u.numel(), generator=g, device=u.device)[:max_values]]
+    table = LevelTable.uniform(bit_width)
+    for _ in range(passes):
+        table = learn_levels(u, table, learning_rate)
+    return table
