@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gpt", action="store_true")
+    ap.add_argument("--no-levels", action="store_true", help="skip the learned-levels kernel timings")
     ap.add_argument("--gpt-steps", type=int, default=8)
     ap.add_argument("--gpt-batch", type=int, default=8, help="sequences per GPU")
     ap.add_argument("--gpt-seq", type=int, default=1024)
@@ -385,6 +386,48 @@ def main():
                     "method": "algorithmic bytes / CUDA-event time of that kernel's launches (graph of one step's "
                               "launches of the kind, L2 flushed between replays)"}
 
+    # ---- learned-levels kernels on the same weight groups (world 1) ----
+    levels = None
+    if world == 1 and not args.no_levels:
+        from paper_2302_02390_b200.levels import LevelTable, dequantize_levels, learn_levels, quantize_levels_segments
+        lspec = QuantSpec(args.wbits, args.bucket, "levels")
+        u = torch.rand(1 << 18, generator=gen, device=dev, dtype=torch.float64)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        table = learn_levels(u, LevelTable.uniform(args.wbits))
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        learn_ms = a.elapsed_time(b)
+        for st in state:
+            st["lq"] = (torch.empty(codes_bytes(st["g"].numel, lspec) + 16, dtype=torch.uint8, device=dev),
+                        torch.empty((num_buckets(st["g"].numel, args.bucket), 3), dtype=torch.float32, device=dev))
+        lbytes = {"LQ_quantize_levels": sum(4 * st["g"].numel + codes_bytes(st["g"].numel, lspec)
+                                            + 12 * num_buckets(st["g"].numel, args.bucket) for st in state),
+                  "LD_dequantize_levels": sum(osz * st["g"].numel + codes_bytes(st["g"].numel, lspec)
+                                              + 12 * num_buckets(st["g"].numel, args.bucket) for st in state)}
+
+        def lq_all():
+            for st in state:
+                quantize_levels_segments([st["shard"]], lspec, table, out=[st["lq"]])
+
+        def ld_all():
+            for st in state:
+                dequantize_levels(st["lq"][0], st["lq"][1], st["g"].numel, lspec, table, dtype=out_dt, out=st["full"])
+
+        levels = {"table": f"{1 << args.wbits} levels learned (Alg. 2) on 2^18 uniform values",
+                  "learn_levels_values_per_s": round(u.numel() / (learn_ms * 1e-3), 1)}
+        for name, fn in (("LQ_quantize_levels", lq_all), ("LD_dequantize_levels", ld_all)):
+            fn()
+            gk = capture(fn)
+            gk.replay()
+            torch.cuda.synchronize(dev)
+            evk = time_graph(gk, args.steps)
+            torch.cuda.synchronize(dev)
+            tk = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+            levels[name] = {"ms_per_pass": round(tk, 4), "gbs": round(lbytes[name] / (tk * 1e-3) / 1e9, 1),
+                            "frac_of_hbm_peak": round(lbytes[name] / (tk * 1e-3) / 1e9 / hbm_peak, 4),
+                            "bytes_per_pass": lbytes[name], "launches_per_pass": len(state)}
+
     # ---- e2e: through the C-ABI communicator, host buffers, copies inside the timed region ----
     e2e = None
     if not args.no_e2e:
@@ -466,6 +509,7 @@ def main():
                                     + ("fused single-launch collectives" if comm_fused else "3 launches per collective"),
                        "convention": "sum over ranks of 4*N per collective / time"},
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
+            "levels": levels,
             "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
