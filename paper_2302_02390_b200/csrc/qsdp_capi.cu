@@ -129,6 +129,8 @@ struct DynSrc {
   const unsigned long long* parity_ptr = nullptr;  // slot parity = (*parity_ptr + adj) & 1
   int64_t parity_stride = 0;
   int32_t parity_adj = 0;
+  int32_t mirror_n = 0;  // push collectives: copy every bucket to these byte offsets too
+  int64_t mirror_delta[QSDP_FUSE_MAX_WORLD - 1] = {};
 };
 
 // Table builders shared by the launch-per-stage path and the fused collectives.
@@ -143,6 +145,8 @@ void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, co
   tab.parity_ptr = dyn.parity_ptr;
   tab.parity_stride = dyn.parity_stride;
   tab.parity_adj = dyn.parity_adj;
+  tab.mirror_n = dyn.mirror_n;
+  for (int k = 0; k < dyn.mirror_n; ++k) tab.mirror_delta[k] = dyn.mirror_delta[k];
   int64_t nb = 0;
   vec = cfg->bucket % 4 == 0;
   int nj = 0;
@@ -737,6 +741,15 @@ static bool fused_cfg_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype)
          cfg->bucket * 4 <= 8192;
 }
 
+// The push all-gather needs the quantizer that copies buckets out (the TMA32
+// kernel: direct widths, S % 8 == 0, 72 <= S, S * sizeof(T) <= 8 KB).
+static bool push_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
+  const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
+  const int isz = in_dtype == QSDP_F64 ? 8 : 4;
+  return c->world > 1 && cfg->inner != QSDP_INNER_LEVELS && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 72 &&
+         cfg->bucket * isz <= 8192;
+}
+
 static FuseSync comm_sync(const qsdp_comm* c) {
   FuseSync fs;
   memset(&fs, 0, sizeof(fs));
@@ -799,6 +812,28 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
     st = try_fused(c, q, d, cfg, 0, 1, out_dtype, s, launched);
     if (st != QSDP_OK || launched) return st;
   }
+  if (push_ok(c, cfg, in_dtype)) {
+    // PUSH: the quantizer writes this rank's shard into slot [rank] of its own
+    // workspace and, bucket by bucket, copies it to slot [rank] of every peer
+    // (NVLink stores overlapped with the quantizer); after the barrier every
+    // rank dequantizes all P slots from its own HBM.
+    q[0].codes = c->slot(c->base, c->rank);
+    q[0].meta = reinterpret_cast<float*>(q[0].codes + c->slot_codes);
+    DynSrc dq = comm_dyn(c, 1);
+    for (int p = 0; p < c->world; ++p)
+      if (p != c->rank) dq.mirror_delta[dq.mirror_n++] = (int64_t)((uintptr_t)c->peer[p] - (uintptr_t)c->base);
+    for (int p = 0; p < c->world; ++p) {
+      uint8_t* sl = c->slot(c->base, p);
+      d[p].codes[0] = sl;
+      d[p].meta[0] = reinterpret_cast<const float*>(sl + c->slot_codes);
+    }
+    st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
+    if (st != QSDP_OK) return st;
+    st = comm_barrier(c, s);
+    if (st != QSDP_OK) return st;
+    return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0));
+  }
+  // PULL (other configurations): quantize into the local slot [0]; peers read it
   // 1. quantize this rank's shard into its local slot (key worker 0, sharded.py:341)
   st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1), lv ? c->wlevels : nullptr, c->wnlevels);
   if (st != QSDP_OK) return st;
@@ -840,13 +875,28 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
     st = try_fused(c, q, d, cfg, 1, c->world, out_dtype, s, launched);
     if (st != QSDP_OK || launched) return st;
   }
+  // Launch-per-stage path: PUSH.  The quantizer stores destination q's codes
+  // straight into owner q's receive slot [rank] over NVLink (K2 is compute-bound,
+  // so the posted peer stores ride along), and the owner's dequant-accumulate
+  // then reads all P sources from its own HBM.  Slot reuse is safe with the same
+  // barrier: a rank writes parity n's slots on a peer only after that peer has
+  // arrived at barrier n-1, which it does after finishing its dequant of call n-2.
+  for (int p = 0; p < c->world; ++p) {
+    q[p].codes = c->slot(c->peer[p], c->rank);
+    q[p].meta = reinterpret_cast<float*>(q[p].codes + c->slot_codes);
+  }
+  for (int p = 0; p < c->world; ++p) {
+    uint8_t* sl = c->slot(c->base, p);
+    d[0].codes[p] = sl;
+    d[0].meta[p] = reinterpret_cast<const float*>(sl + c->slot_codes);
+  }
   st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
   if (st != QSDP_OK) return st;
   if (c->world > 1) {
     st = comm_barrier(c, s);
     if (st != QSDP_OK) return st;
   }
-  // 3. owner pulls its segment from sources 0..P-1 (in order) and accumulates
+  // 3. owner dequant-accumulates sources 0..P-1 (in order) from its own slots
   return run_dequant(d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 0));
 }
 

@@ -214,7 +214,10 @@ struct QJobTable {
   const unsigned long long* parity_ptr;
   int64_t parity_stride;
   int32_t parity_adj;
-  int32_t _pad3;
+  // push collectives: every bucket's codes + meta are also copied to
+  // (its address + mirror_delta[k]) -- the same slot in a peer's workspace
+  int32_t mirror_n;
+  int64_t mirror_delta[QSDP_FUSE_MAX_WORLD - 1];
 };
 
 struct DJob {

@@ -584,6 +584,26 @@ __device__ __forceinline__ void store_octet(uint8_t* base, int o, uint64_t w) {
   else base[o] = (uint8_t)w;  // BITS == 16 never takes the octet path (64-bit word holds 4 codes)
 }
 
+// Push collectives: after the warp has written bucket codes (cb, nbytes) and its
+// meta (m), copy both to the same offsets in every peer workspace
+// (address + tab.mirror_delta[k], NVLink stores).  __syncwarp() has ordered the
+// warp's own stores; the re-read comes from L2 (ld.cg), 16 bytes per lane.
+__device__ __forceinline__ void mirror_bucket(const QJobTable& tab, uint8_t* cb, int64_t nbytes, float* m, int lane) {
+  const int64_t head = ((uintptr_t)cb & 15) ? 0 : (nbytes >> 4);
+  for (int64_t i = lane; i < head; i += 32) {
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(cb) + i);
+    for (int k = 0; k < tab.mirror_n; ++k) reinterpret_cast<uint4*>(cb + tab.mirror_delta[k])[i] = v;
+  }
+  for (int64_t i = (head << 4) + lane; i < nbytes; i += 32) {
+    const uint8_t v = __ldcg(cb + i);
+    for (int k = 0; k < tab.mirror_n; ++k) cb[tab.mirror_delta[k] + i] = v;
+  }
+  if (lane < 3) {
+    const float v = __ldcg(m + lane);
+    for (int k = 0; k < tab.mirror_n; ++k) meta_at(m, tab.mirror_delta[k])[lane] = v;
+  }
+}
+
 // Rare path of the octet loop: recompute the 8 codes, certifying each element
 // again and falling back to the exact chain where the bound is not met.
 template <typename T, int BITS>
@@ -913,6 +933,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
       m[2] = hif;
     }
     __syncwarp();
+    if (tab.mirror_n > 0) mirror_bucket(tab, cbase, payload_bytes(n, BITS), meta_at(J.meta, poff) + 3 * br.lb, lane);
     fence_proxy_async();
     if (bucket_of(k + NST) < total) issue(k + NST);
   }
@@ -1285,6 +1306,86 @@ __device__ __forceinline__ void dequant_fast32(const DJobTable& tab, int64_t pof
   }
 }
 
+// K4 fast path for nsrc in [2, NSMAX]: one warp per bucket (S % 128 == 0,
+// S <= 1024, direct widths 8 / 4, aligned buffers).  The code words of ALL
+// sources for a chunk of UC groups per lane are issued together (NSMAX * UC = 16
+// loads in flight per lane) before the ordered fp64 accumulation
+// (acc = 0.0; acc = acc + val_p for p = 0..nsrc-1; acc / divisor, sharded.py:385-431).
+// Per-source scales live in shared memory rows (lanes < nsrc fill them).
+// A power-of-two divisor is applied as a multiply by its exact reciprocal
+// (bit-identical to the division); other divisors divide.
+template <int BITS, int OUT, bool COH, int NSMAX>
+__device__ __forceinline__ void dequant_acc_fast32(const DJobTable& tab, int64_t poff, int64_t warp, int64_t nwarps,
+                                                   double (*row)[3]) {
+  constexpr int UC = 16 / NSMAX;
+  const int lane = threadIdx.x & 31;
+  const int S = tab.bucket;
+  const int G = S >> 7;  // groups per lane
+  const double top = (double)((1u << BITS) - 1u);
+  const int64_t pbs = payload_bytes(S, BITS);
+  const int dv = tab.divisor;
+  const bool pow2 = (dv & (dv - 1)) == 0;
+  const double rdiv = 1.0 / (double)dv;  // exact for powers of two
+  for (int64_t b = warp; b < tab.total_buckets; b += nwarps) {
+    const int j = find_job_d(tab, b);
+    const DJob& J = tab.jobs[j];
+    const int nsrc = J.nsrc;
+    const int64_t lb = b - J.bucket_base, off = lb * S;
+    const int n = (int)min((int64_t)S, J.length - off);
+    __syncwarp();
+    if (lane < nsrc) {
+      const float* m = meta_at(J.meta[lane], poff) + 3 * lb;
+      const float m0 = COH ? __ldcg(m) : m[0], m1 = COH ? __ldcg(m + 1) : m[1], m2 = COH ? __ldcg(m + 2) : m[2];
+      const double lo = (double)m1;
+      row[lane][0] = lo;
+      row[lane][1] = __ddiv_rn(__dsub_rn((double)m2, lo), top);  // QuantizedBlock.pitch
+      row[lane][2] = (double)m0;
+    }
+    __syncwarp();
+    for (int g0 = 0; g0 < G; g0 += UC) {
+      uint32_t w[NSMAX][UC];
+#pragma unroll
+      for (int p = 0; p < NSMAX; ++p) {
+        const uint8_t* __restrict__ cp = J.codes[p < nsrc ? p : 0] + poff + lb * pbs;
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+          const int gi = (g0 + u) * 32 + lane;
+          w[p][u] = (p < nsrc && g0 + u < G && 4 * gi < n) ? (uint32_t)load_group_direct<BITS, COH>(cp, gi) : 0u;
+        }
+      }
+      double acc[UC][4];
+#pragma unroll
+      for (int u = 0; u < UC; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[u][i] = 0.0;
+#pragma unroll
+      for (int p = 0; p < NSMAX; ++p) {
+        if (p < nsrc) {
+          const double lo = row[p][0], pitch = row[p][1], shift = row[p][2];
+#pragma unroll
+          for (int u = 0; u < UC; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const double c = code_to_double((w[p][u] >> (i * BITS)) & ((1u << BITS) - 1u));
+              acc[u][i] = __dadd_rn(acc[u][i], __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift));
+            }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int gi = (g0 + u) * 32 + lane;
+        const int e = 4 * gi;
+        if (g0 + u < G && e < n) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            acc[u][i] = pow2 ? __dmul_rn(acc[u][i], rdiv) : __ddiv_rn(acc[u][i], (double)dv);
+          store_out4<OUT, true>(J.out, off + e, n - e, acc[u]);
+        }
+      }
+    }
+  }
+}
+
 template <int BITS, int TL, int OUT, bool VEC, bool ACC, bool COH = false>
 __device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_meta_base) {
   const int64_t poff = d_parity_off(tab);
@@ -1316,6 +1417,17 @@ __device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_me
     if (single && cvec && (S & 127) == 0 && S <= 1024) {
       dequant_fast32<BITS, OUT, COH, ACC>(tab, poff, warp, nwarps);
       return;
+    }
+    if constexpr (ACC) {
+      int ns = 0;
+      for (int j = 0; j < tab.njobs; ++j) ns = max(ns, tab.jobs[j].nsrc);
+      if (cvec && (S & 127) == 0 && S <= 1024 && ns <= 8) {
+        double(*row)[3] = reinterpret_cast<double(*)[3]>(sm_meta_base + ((size_t)wib * TEAMS * 8) * 3);
+        if (ns <= 2) dequant_acc_fast32<BITS, OUT, COH, 2>(tab, poff, warp, nwarps, row);
+        else if (ns <= 4) dequant_acc_fast32<BITS, OUT, COH, 4>(tab, poff, warp, nwarps, row);
+        else dequant_acc_fast32<BITS, OUT, COH, 8>(tab, poff, warp, nwarps, row);
+        return;
+      }
     }
   }
 
