@@ -765,7 +765,7 @@ static FuseSync comm_sync(const qsdp_comm* c) {
 // Returns QSDP_OK if launched, QSDP_EINVAL (silently) if the fused path does not apply.
 static qsdp_status try_fused(qsdp_comm* c, const std::vector<QJobSpec>& q, const std::vector<DJobSpec>& d,
                              const qsdp_qcfg* cfg, int accumulate, int divisor, int out_dtype, cudaStream_t s,
-                             bool& launched) {
+                             const DynSrc& qdyn, bool& launched) {
   launched = false;
   for (int j = 0; j < c->world; ++j)
     if (c->peer[j] == nullptr) return fail(QSDP_EPEER, "peers not opened");
@@ -773,7 +773,7 @@ static qsdp_status try_fused(qsdp_comm* c, const std::vector<QJobSpec>& q, const
   DJobTable dt;
   size_t qi = 0, di = 0;
   bool qvec = false, dvec = false;
-  build_qtab(qt, q, qi, cfg, nullptr, comm_dyn(c, 1), qvec);
+  build_qtab(qt, q, qi, cfg, nullptr, qdyn, qvec);
   build_dtab(dt, d, di, cfg, accumulate, divisor, out_dtype, comm_dyn(c, 0), dvec);
   if (qi != q.size() || di != d.size() || !dvec || !dt.codes_vec) return QSDP_OK;
   if (out_dtype != QSDP_F32 && !(out_dtype == QSDP_BF16 && !accumulate)) return QSDP_OK;
@@ -795,12 +795,24 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
   const qsdp_qcfg* cfg = &c->w;
   const bool lv = cfg->inner == QSDP_INNER_LEVELS;
   if (lv && c->wlevels == nullptr) return fail(QSDP_EINVAL, "inner 'levels' requires a LevelTable (qsdp_comm_set_weight_levels)");
-  std::vector<QJobSpec> q(1, comm_qjob(shard, segs[c->rank], c->slot(c->base, 0), c->slot_codes, *key, 0));
+  const bool push = push_ok(c, cfg, in_dtype);
+  // PUSH: the quantizer writes this rank's shard into slot [rank] of its own
+  // workspace and, bucket by bucket, copies it to slot [rank] of every peer
+  // (NVLink stores overlapped with the quantizer); after the barrier every rank
+  // dequantizes all P slots from its own HBM.
+  // PULL (other configurations): quantize into the local slot [0]; after the
+  // barrier every rank dequantizes the P shards straight from the peers' slots.
+  DynSrc dq = comm_dyn(c, 1);
+  if (push)
+    for (int p = 0; p < c->world; ++p)
+      if (p != c->rank) dq.mirror_delta[dq.mirror_n++] = (int64_t)((uintptr_t)c->peer[p] - (uintptr_t)c->base);
+  std::vector<QJobSpec> q(1, comm_qjob(shard, segs[c->rank], c->slot(c->base, push ? c->rank : 0), c->slot_codes,
+                                       *key, 0));  // key worker 0 (sharded.py:341)
   std::vector<DJobSpec> d(c->world);
   const size_t osz = dtype_size(out_dtype);
   for (int p = 0; p < c->world; ++p) {
     memset(&d[p], 0, sizeof(DJobSpec));
-    uint8_t* sl = c->slot(c->peer[p], 0);
+    uint8_t* sl = push ? c->slot(c->base, p) : c->slot(c->peer[p], 0);
     d[p].codes[0] = sl;
     d[p].meta[0] = reinterpret_cast<const float*>(sl + c->slot_codes);
     d[p].nsrc = 1;
@@ -809,40 +821,18 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
   }
   if (fused_cfg_ok(c, cfg, in_dtype)) {
     bool launched = false;
-    st = try_fused(c, q, d, cfg, 0, 1, out_dtype, s, launched);
+    st = try_fused(c, q, d, cfg, 0, 1, out_dtype, s, dq, launched);
     if (st != QSDP_OK || launched) return st;
   }
-  if (push_ok(c, cfg, in_dtype)) {
-    // PUSH: the quantizer writes this rank's shard into slot [rank] of its own
-    // workspace and, bucket by bucket, copies it to slot [rank] of every peer
-    // (NVLink stores overlapped with the quantizer); after the barrier every
-    // rank dequantizes all P slots from its own HBM.
-    q[0].codes = c->slot(c->base, c->rank);
-    q[0].meta = reinterpret_cast<float*>(q[0].codes + c->slot_codes);
-    DynSrc dq = comm_dyn(c, 1);
-    for (int p = 0; p < c->world; ++p)
-      if (p != c->rank) dq.mirror_delta[dq.mirror_n++] = (int64_t)((uintptr_t)c->peer[p] - (uintptr_t)c->base);
-    for (int p = 0; p < c->world; ++p) {
-      uint8_t* sl = c->slot(c->base, p);
-      d[p].codes[0] = sl;
-      d[p].meta[0] = reinterpret_cast<const float*>(sl + c->slot_codes);
-    }
-    st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
-    if (st != QSDP_OK) return st;
-    st = comm_barrier(c, s);
-    if (st != QSDP_OK) return st;
-    return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0));
-  }
-  // PULL (other configurations): quantize into the local slot [0]; peers read it
-  // 1. quantize this rank's shard into its local slot (key worker 0, sharded.py:341)
-  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1), lv ? c->wlevels : nullptr, c->wnlevels);
+  // 1. quantize this rank's shard (and push it when `push`)
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, dq, lv ? c->wlevels : nullptr, c->wnlevels);
   if (st != QSDP_OK) return st;
   // 2. publish + wait for every peer's slot of this call
   if (c->world > 1) {
     st = comm_barrier(c, s);
     if (st != QSDP_OK) return st;
   }
-  // 3. pull-dequantize all P shards over NVLink into the gathered buffer
+  // 3. dequantize all P shards into the gathered buffer
   return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0), lv ? c->wlevels : nullptr);
 }
 
@@ -854,16 +844,22 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const qsdp_qcfg* cfg = &c->g;
   const size_t isz = dtype_size(in_dtype);
+  // PUSH: the quantizer stores destination q's codes straight into owner q's
+  // receive slot [rank] over NVLink (K2 is compute-bound, so the posted peer
+  // stores ride along), and the owner's dequant-accumulate reads all P sources
+  // from its own HBM.  Slot reuse is safe with one barrier per collective: a rank
+  // writes parity n's slots on a peer only after that peer has arrived at
+  // barrier n-1, which it does after finishing its dequant of call n-2.
   // 1. quantize every destination segment of this rank's gradient (worker = rank)
   std::vector<QJobSpec> q;
   for (int p = 0; p < c->world; ++p) {
     const void* x = static_cast<const uint8_t*>(full_grad) + (size_t)(segs[p].global_start - segs[0].global_start) * isz;
-    q.push_back(comm_qjob(x, segs[p], c->slot(c->base, p), c->slot_codes, *key, (uint64_t)c->rank));
+    q.push_back(comm_qjob(x, segs[p], c->slot(c->peer[p], c->rank), c->slot_codes, *key, (uint64_t)c->rank));
   }
   std::vector<DJobSpec> d(1);
   memset(&d[0], 0, sizeof(DJobSpec));
   for (int p = 0; p < c->world; ++p) {
-    uint8_t* sl = c->slot(c->peer[p], c->rank);
+    uint8_t* sl = c->slot(c->base, p);
     d[0].codes[p] = sl;
     d[0].meta[p] = reinterpret_cast<const float*>(sl + c->slot_codes);
   }
@@ -872,23 +868,8 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
   d[0].out = shard_out;
   if (fused_cfg_ok(c, cfg, in_dtype)) {
     bool launched = false;
-    st = try_fused(c, q, d, cfg, 1, c->world, out_dtype, s, launched);
+    st = try_fused(c, q, d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 1), launched);
     if (st != QSDP_OK || launched) return st;
-  }
-  // Launch-per-stage path: PUSH.  The quantizer stores destination q's codes
-  // straight into owner q's receive slot [rank] over NVLink (K2 is compute-bound,
-  // so the posted peer stores ride along), and the owner's dequant-accumulate
-  // then reads all P sources from its own HBM.  Slot reuse is safe with the same
-  // barrier: a rank writes parity n's slots on a peer only after that peer has
-  // arrived at barrier n-1, which it does after finishing its dequant of call n-2.
-  for (int p = 0; p < c->world; ++p) {
-    q[p].codes = c->slot(c->peer[p], c->rank);
-    q[p].meta = reinterpret_cast<float*>(q[p].codes + c->slot_codes);
-  }
-  for (int p = 0; p < c->world; ++p) {
-    uint8_t* sl = c->slot(c->base, p);
-    d[0].codes[p] = sl;
-    d[0].meta[p] = reinterpret_cast<const float*>(sl + c->slot_codes);
   }
   st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
   if (st != QSDP_OK) return st;
