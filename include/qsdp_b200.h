@@ -19,7 +19,9 @@
  *   dequantize  quantize.py:209-232                    qsdp_dequantize / qsdp_dequantize_batch
  *   acc = acc + vals ... acc / P  sharded.py:385-431   qsdp_dequant_accumulate
  *   message_size_bits  wire.py:187-192                 qsdp_message_size_bits
- *   encode  wire.py:108-131                            qsdp_wire_encode (host export of one segment)
+ *   encode  wire.py:108-131                            qsdp_wire_encode_device (device) /
+ *                                                        qsdp_wire_encode (host buffers)
+ *   decode  wire.py:134-184                            qsdp_wire_parse + qsdp_wire_decode_device
  *   ShardedMLP._gather  sharded.py:323-373             qsdp_all_gather (one process per GPU)
  *   ShardedMLP._reduce_scatter  sharded.py:375-433     qsdp_reduce_scatter
  *   quantize_bucket (levels) + quantize_with_levels    qsdp_quantize_levels / _batch
@@ -37,7 +39,9 @@
  *   QSDP_EINVAL     ValueError for bad arguments (bit width, bucket size, ...)
  *   QSDP_ENONFINITE ValueError("non-finite ... at index i") -- reported through
  *                   the optional device word *d_bad (see qsdp_quantize)
- *   QSDP_ERANGE     CodeRangeError / DecodeError (qsdp_wire_decode)
+ *   QSDP_ERANGE     CodeRangeError (wire.py:74; header bit width outside [1, 32])
+ *   QSDP_EDECODE / QSDP_ETRUNC / QSDP_EVERSION   DecodeError / TruncatedMessageError /
+ *                   UnsupportedVersionError (qsdp_wire_parse / qsdp_wire_decode_device)
  *   QSDP_ECUDA      CUDA runtime failure (message in qsdp_last_error())
  *   QSDP_EPEER      peer-memory / IPC setup failure
  */
@@ -58,7 +62,10 @@ typedef enum {
   QSDP_ERANGE = 3,
   QSDP_ECUDA = 4,
   QSDP_ENCCL = 5,
-  QSDP_EPEER = 6
+  QSDP_EPEER = 6,
+  QSDP_EDECODE = 7,   /* DecodeError (wire.py:62) */
+  QSDP_ETRUNC = 8,    /* TruncatedMessageError (wire.py:66) */
+  QSDP_EVERSION = 9   /* UnsupportedVersionError (wire.py:70) */
 } qsdp_status;
 
 typedef enum { QSDP_INNER_SHIFT = 0, QSDP_INNER_STOCHASTIC = 1, QSDP_INNER_LEVELS = 2 } qsdp_inner;
@@ -176,6 +183,35 @@ qsdp_status qsdp_dequantize_levels(const uint8_t* codes, const float* meta, int6
  * nlevels: a power of two <= 4096. */
 qsdp_status qsdp_learn_levels(const double* d_values, int64_t n, double* d_levels, int32_t nlevels,
                               double learning_rate, void* stream);
+
+/* ---- wire codec: byte-exact reference messages ---- */
+typedef struct {
+  int32_t version, bits;
+  int64_t bucket, blocks, total_length;
+  int64_t expected_bytes;   /* size of a well-formed message with this header */
+  int64_t complete_blocks;  /* leading blocks wholly present in msg_bytes */
+} qsdp_wire_info;
+/* Header parse with decode's header-level checks, in its order (wire.py:136-158):
+ * hdr = the first min(14, msg_bytes) bytes (host).  QSDP_OK with blocks == 0 for the
+ * empty message.  Truncation / trailing bytes are reported by the caller after the
+ * complete blocks were validated (info->complete_blocks, info->expected_bytes). */
+qsdp_status qsdp_wire_parse(const uint8_t* hdr, int64_t msg_bytes, qsdp_wire_info* info);
+/* Device encode: one segment in the device layout -> the message
+ * (qsdp_message_size_bits(length, cfg) / 8 bytes at d_out). */
+qsdp_status qsdp_wire_encode_device(const uint8_t* codes, const float* meta, int64_t length,
+                                    const qsdp_qcfg* cfg, uint8_t* d_out, int64_t out_cap, void* stream);
+/* Device decode of info->complete_blocks blocks into the device layout (any
+ * width 1..32; the quantizers / dequantizers use 1..16).  d_err[2] (device, init UINT64_MAX) receive the first block with nonzero
+ * padding bits (DecodeError) and the first with !(scale_lo <= scale_hi) (ValueError). */
+qsdp_status qsdp_wire_decode_device(const uint8_t* d_msg, const qsdp_wire_info* info, uint8_t* codes,
+                                    float* meta, uint64_t* d_err, void* stream);
+
+/* uint32 codes (one per element, < 2^bits) <-> the packed device layout
+ * (_pack_codes / _unpack_codes per bucket, wire.py:82-95), widths 1..32. */
+qsdp_status qsdp_pack_codes(const uint32_t* codes, int64_t length, const qsdp_qcfg* cfg, uint8_t* out,
+                            void* stream);
+qsdp_status qsdp_unpack_codes(const uint8_t* packed, int64_t length, const qsdp_qcfg* cfg, uint32_t* codes,
+                              void* stream);
 
 /* ---- host wire export (wire.py:108-131): codes/meta already on the host ---- */
 int64_t qsdp_wire_encode(const uint8_t* codes, const float* meta, int64_t length,

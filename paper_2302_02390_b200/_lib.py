@@ -21,6 +21,9 @@ QSDP_ERANGE = 3
 QSDP_ECUDA = 4
 QSDP_ENCCL = 5
 QSDP_EPEER = 6
+QSDP_EDECODE = 7
+QSDP_ETRUNC = 8
+QSDP_EVERSION = 9
 
 INNER_SHIFT = 0
 INNER_STOCHASTIC = 1
@@ -38,6 +41,8 @@ EXPORTED_SYMBOLS = (
     "qsdp_counter_add", "qsdp_comm_set_step_source", "qsdp_comm_set_fused",
     "qsdp_quantize_levels", "qsdp_quantize_levels_batch", "qsdp_dequantize_levels",
     "qsdp_dequantize_levels_batch", "qsdp_learn_levels", "qsdp_comm_set_weight_levels",
+    "qsdp_wire_parse", "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes",
+    "qsdp_unpack_codes",
 )
 
 
@@ -66,8 +71,39 @@ class DItem(ctypes.Structure):
                 ("nsrc", ctypes.c_int32), ("length", ctypes.c_int64), ("out", ctypes.c_void_p)]
 
 
+class WireInfo(ctypes.Structure):
+    _fields_ = [("version", ctypes.c_int32), ("bits", ctypes.c_int32), ("bucket", ctypes.c_int64),
+                ("blocks", ctypes.c_int64), ("total_length", ctypes.c_int64), ("expected_bytes", ctypes.c_int64),
+                ("complete_blocks", ctypes.c_int64)]
+
+
 class QSDPError(RuntimeError):
     """CUDA / peer failure inside the native library."""
+
+
+# The reference's wire exception hierarchy (wire.py:54-75).
+class WireError(ValueError):
+    pass
+
+
+class EncodeError(WireError):
+    pass
+
+
+class DecodeError(WireError):
+    pass
+
+
+class TruncatedMessageError(DecodeError):
+    pass
+
+
+class UnsupportedVersionError(DecodeError):
+    pass
+
+
+class CodeRangeError(DecodeError):
+    pass
 
 
 _lib = None
@@ -109,6 +145,11 @@ def lib():
     L.qsdp_comm_set_step_source.argtypes = [vp, vp]
     L.qsdp_comm_set_fused.argtypes = [vp, i32]
     L.qsdp_comm_set_weight_levels.argtypes = [vp, vp, i32]
+    L.qsdp_wire_parse.argtypes = [vp, i64, ctypes.POINTER(WireInfo)]
+    L.qsdp_wire_encode_device.argtypes = [vp, vp, i64, cfgp, vp, i64, vp]
+    L.qsdp_wire_decode_device.argtypes = [vp, ctypes.POINTER(WireInfo), vp, vp, vp, vp]
+    L.qsdp_pack_codes.argtypes = [vp, i64, cfgp, vp, vp]
+    L.qsdp_unpack_codes.argtypes = [vp, i64, cfgp, vp, vp]
     L.qsdp_dequantize.argtypes = [vp, vp, i64, cfgp, vp, i32, vp]
     L.qsdp_dequantize_batch.argtypes = [ctypes.POINTER(DItem), i32, cfgp, i32, vp]
     L.qsdp_dequant_accumulate.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i64, cfgp,
@@ -133,7 +174,8 @@ def lib():
                  "qsdp_comm_ipc_handle", "qsdp_comm_open_peers", "qsdp_all_gather",
                  "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_levels",
                  "qsdp_quantize_levels_batch", "qsdp_dequantize_levels", "qsdp_dequantize_levels_batch",
-                 "qsdp_learn_levels", "qsdp_comm_set_weight_levels"):
+                 "qsdp_learn_levels", "qsdp_comm_set_weight_levels", "qsdp_wire_parse",
+                 "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes", "qsdp_unpack_codes"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib
@@ -147,5 +189,11 @@ def check(status: int) -> None:
     if status in (QSDP_EINVAL, QSDP_ENONFINITE):
         raise ValueError(msg)
     if status == QSDP_ERANGE:
-        raise ValueError(msg)
+        raise CodeRangeError(msg)
+    if status == QSDP_EDECODE:
+        raise DecodeError(msg)
+    if status == QSDP_ETRUNC:
+        raise TruncatedMessageError(msg)
+    if status == QSDP_EVERSION:
+        raise UnsupportedVersionError(msg)
     raise QSDPError(f"qsdp status {status}: {msg}")

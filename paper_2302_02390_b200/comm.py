@@ -87,6 +87,35 @@ def sent_bits(kind: str, rank: int, world: int, segs, spec: QuantSpec) -> int:
     return sum(message_size_bits(segs[q][1], spec) for q in range(world) if q != rank and segs[q][1] > 0)
 
 
+def record_allgather(entry, layer: str, segs, spec: QuantSpec) -> None:
+    """The reference's ledger records of one quantized all-gather
+    (sharded.py:349-358): one message per non-empty shard, world-1 copies."""
+    from .quantize import message_size_bits
+    from .sharded import Transfer
+    world = len(segs)
+    for _, n in segs:
+        if n > 0:
+            entry.record(Transfer("allgather", layer, spec.bits, message_size_bits(n, spec) // 8, world - 1,
+                                  n * spec.bits))
+    entry.allgather_events += 1
+
+
+def record_reducescatter(entry, layer: str, segs, spec: QuantSpec) -> None:
+    """The reference's ledger records of one quantized reduce-scatter
+    (sharded.py:403-413): every (source p, destination q != p) segment message."""
+    from .quantize import message_size_bits
+    from .sharded import Transfer
+    world = len(segs)
+    for q, (_, n) in enumerate(segs):
+        if n == 0:
+            continue
+        for p in range(world):
+            if p != q:
+                entry.record(Transfer("reducescatter", layer, spec.bits, message_size_bits(n, spec) // 8, 1,
+                                      n * spec.bits))
+    entry.reducescatter_events += 1
+
+
 class QSDPComm:
     """NVLink peer-memory communicator for QSDP's quantized AG / RS."""
 

@@ -39,6 +39,14 @@ cudaError_t launch_quantize_levels(const QJobTable& tab, int in_f64, const doubl
                                    cudaStream_t s);
 cudaError_t launch_dequant_levels(const DJobTable& tab, const double* levels, bool vec, int sms, cudaStream_t s);
 cudaError_t launch_learn_levels(const double* values, int64_t n, double* q, int nl, double lr, cudaStream_t s);
+cudaError_t launch_wire_encode(const uint8_t* codes, const float* meta, const WireGeom& g, uint8_t* out, int sms,
+                               cudaStream_t s);
+cudaError_t launch_wire_decode(const uint8_t* msg, const WireGeom& g, int64_t nblk, uint8_t* codes, float* meta,
+                               unsigned long long* err, int sms, cudaStream_t s);
+cudaError_t launch_pack_codes(const uint32_t* codes, int64_t length, int bucket, int bits, uint8_t* out,
+                              int64_t out_bytes, int sms, cudaStream_t s);
+cudaError_t launch_unpack_codes(const uint8_t* packed, int64_t length, int bucket, int bits, uint32_t* codes, int sms,
+                                cudaStream_t s);
 }  // namespace qsdp
 
 using namespace qsdp;
@@ -475,6 +483,136 @@ qsdp_status qsdp_dequant_accumulate(const uint8_t* const* codes, const float* co
 qsdp_status qsdp_dequant_accumulate_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
                                           int32_t divisor, int32_t out_dtype, void* stream) {
   return dequant_items(items, nitems, cfg, 1, divisor, out_dtype, stream);
+}
+
+static void put_u32_le(uint8_t* p, uint32_t v) { memcpy(p, &v, 4); }
+static uint32_t get_u32_le(const uint8_t* p) {
+  uint32_t v;
+  memcpy(&v, p, 4);
+  return v;
+}
+
+// Geometry of a message with this header (all blocks full but the last).
+static WireGeom wire_geom(int bits, int64_t bucket, int64_t nb, int64_t total) {
+  WireGeom g;
+  memset(&g, 0, sizeof(g));
+  g.bits = bits;
+  g.bucket = (int32_t)bucket;
+  g.length = total;
+  g.nb = nb;
+  g.pbs = payload(bucket, bits);
+  g.last_n = total - (nb - 1) * bucket;
+  g.last_pb = payload(g.last_n, bits);
+  g.blk = 12 + g.pbs;
+  g.msg_bytes = 14 + (nb - 1) * g.blk + 12 + g.last_pb;
+  g.codes_bytes = (nb - 1) * g.pbs + g.last_pb;
+  g.header[0] = 1;
+  g.header[1] = (uint8_t)bits;
+  put_u32_le(g.header + 2, (uint32_t)(nb == 1 ? total : bucket));
+  put_u32_le(g.header + 6, (uint32_t)nb);
+  put_u32_le(g.header + 10, (uint32_t)total);
+  return g;
+}
+
+qsdp_status qsdp_pack_codes(const uint32_t* codes, int64_t length, const qsdp_qcfg* cfg, uint8_t* out,
+                            void* stream) {
+  if (cfg == nullptr || cfg->bits < 1 || cfg->bits > 32 || cfg->bucket < 1 || length < 0)
+    return fail(QSDP_EINVAL, "bad packing configuration");
+  int sms = 0;
+  qsdp_status st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  cudaError_t e = launch_pack_codes(codes, length, cfg->bucket, cfg->bits, out, qsdp_codes_bytes(length, cfg), sms,
+                                    reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pack launch");
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_unpack_codes(const uint8_t* packed, int64_t length, const qsdp_qcfg* cfg, uint32_t* codes,
+                              void* stream) {
+  if (cfg == nullptr || cfg->bits < 1 || cfg->bits > 32 || cfg->bucket < 1 || length < 0)
+    return fail(QSDP_EINVAL, "bad packing configuration");
+  int sms = 0;
+  qsdp_status st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  cudaError_t e = launch_unpack_codes(packed, length, cfg->bucket, cfg->bits, codes, sms,
+                                      reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "unpack launch");
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_wire_parse(const uint8_t* hdr, int64_t msg_bytes, qsdp_wire_info* info) {
+  if (info == nullptr || (hdr == nullptr && msg_bytes > 0)) return fail(QSDP_EINVAL, "null argument");
+  memset(info, 0, sizeof(*info));
+  if (msg_bytes < 14)
+    return fail(QSDP_ETRUNC, "message of " + std::to_string(msg_bytes) + " bytes is shorter than the header");
+  const int version = hdr[0], bits = hdr[1];
+  const int64_t bucket = get_u32_le(hdr + 2), count = get_u32_le(hdr + 6), total = get_u32_le(hdr + 10);
+  info->version = version;
+  info->bits = bits;
+  info->bucket = bucket;
+  info->blocks = count;
+  info->total_length = total;
+  if (version != 1) return fail(QSDP_EVERSION, "unsupported wire version " + std::to_string(version));
+  if (count == 0) {
+    if (msg_bytes != 14 || total != 0) return fail(QSDP_EDECODE, "empty message carries trailing data");
+    info->expected_bytes = 14;
+    return QSDP_OK;
+  }
+  if (bits < 1 || bits > 32) return fail(QSDP_ERANGE, "header bit_width " + std::to_string(bits) + " outside [1, 32]");
+  if (bucket < 1) return fail(QSDP_EDECODE, "bucket_size must be positive for non-empty messages");
+  // last_len = total - (count-1)*bucket, exactly (u32 * u32 needs 64 unsigned bits)
+  const __int128 last_len = (__int128)total - (__int128)(count - 1) * (__int128)bucket;
+  if (!(last_len >= 1 && last_len <= bucket))
+    return fail(QSDP_EDECODE, "total_length " + std::to_string(total) + " inconsistent with " + std::to_string(count) +
+                                  " buckets of " + std::to_string(bucket));
+  const WireGeom g = wire_geom(bits, bucket, count, total);
+  info->expected_bytes = g.msg_bytes;
+  // leading blocks whose meta and payload are wholly inside msg_bytes
+  int64_t full = (msg_bytes - 14) / g.blk;
+  if (full > count - 1) full = count - 1;
+  info->complete_blocks = full;
+  if (full == count - 1 && 14 + (count - 1) * g.blk + 12 + g.last_pb <= msg_bytes) info->complete_blocks = count;
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_wire_encode_device(const uint8_t* codes, const float* meta, int64_t length, const qsdp_qcfg* cfg,
+                                    uint8_t* d_out, int64_t out_cap, void* stream) {
+  // the codec moves bytes: any width a QuantizedBlock may carry (1..32)
+  if (cfg == nullptr || cfg->bits < 1 || cfg->bits > 32 || cfg->bucket < 1)
+    return fail(QSDP_EINVAL, "bit_width must be in [1, 32] and bucket_size >= 1");
+  qsdp_status st = QSDP_OK;
+  if (length < 0 || length > 0xffffffffll) return fail(QSDP_EINVAL, "segment length must fit the u32 header field");
+  if (d_out == nullptr) return fail(QSDP_EINVAL, "null output");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (length == 0) {  // encode([]) == header (1, 0, 0, 0, 0) (wire.py:110-111)
+    if (out_cap < 14) return fail(QSDP_EINVAL, "wire buffer too small");
+    const uint8_t h[14] = {1, 0};
+    QSDP_CUDA(cudaMemcpyAsync(d_out, h, 14, cudaMemcpyHostToDevice, s));
+    return QSDP_OK;
+  }
+  const WireGeom g = wire_geom(cfg->bits, cfg->bucket, qsdp_num_buckets(length, cfg->bucket), length);
+  if (out_cap < g.msg_bytes) return fail(QSDP_EINVAL, "wire buffer too small");
+  int sms = 0;
+  st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  cudaError_t e = launch_wire_encode(codes, meta, g, d_out, sms, s);
+  if (e != cudaSuccess) return cuda_fail(e, "wire encode launch");
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_wire_decode_device(const uint8_t* d_msg, const qsdp_wire_info* info, uint8_t* codes, float* meta,
+                                    uint64_t* d_err, void* stream) {
+  if (info == nullptr || d_err == nullptr) return fail(QSDP_EINVAL, "null argument");
+  if (info->blocks == 0 || info->complete_blocks == 0) return QSDP_OK;
+  const WireGeom g = wire_geom(info->bits, info->bucket, info->blocks, info->total_length);
+  int sms = 0;
+  qsdp_status st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  cudaError_t e = launch_wire_decode(d_msg, g, info->complete_blocks, codes, meta,
+                                     reinterpret_cast<unsigned long long*>(d_err), sms,
+                                     reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "wire decode launch");
+  return QSDP_OK;
 }
 
 int64_t qsdp_wire_encode(const uint8_t* codes, const float* meta, int64_t length, const qsdp_qcfg* cfg,

@@ -254,6 +254,20 @@ struct FuseSync {
   int rank, world;
 };
 
+// Geometry of one wire message (qsdp_wire.cu).
+struct WireGeom {
+  int64_t length;      // total elements
+  int64_t nb;          // blocks
+  int64_t pbs;         // payload bytes of a full block
+  int64_t last_n;      // elements of the last block
+  int64_t last_pb;     // payload bytes of the last block
+  int64_t blk;         // 12 + pbs: wire bytes of a full block
+  int64_t msg_bytes;   // 14 + sum over blocks
+  int64_t codes_bytes; // (nb-1)*pbs + last_pb
+  int32_t bits, bucket;
+  uint8_t header[16];  // the 14 header bytes (host-built)
+};
+
 __host__ __device__ __forceinline__ int64_t payload_bytes(int64_t len, int bits) { return (len * bits + 7) / 8; }
 
 __device__ __forceinline__ int find_job_q(const QJobTable& t, int64_t b) {

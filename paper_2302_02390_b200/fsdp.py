@@ -25,9 +25,9 @@ import torch
 import torch.distributed as dist
 from torch.distributed.fsdp._fully_shard._fsdp_api import AllGather, ReduceScatter
 
-from .comm import QSDPComm
+from .comm import QSDPComm, record_allgather, record_reducescatter
 from .quantize import QuantSpec, SegmentKey
-from .sharded import PHASE_GRAD, PHASE_W_BWD, PHASE_W_FWD
+from .sharded import PHASE_GRAD, PHASE_W_BWD, PHASE_W_FWD, CommLedger, LedgerEntry
 
 __all__ = ["QSDPContext", "QSDPAllGather", "QSDPReduceScatter", "apply_qsdp"]
 
@@ -51,6 +51,9 @@ class QSDPContext:
         self.step = 0
         self.phase = PHASE_W_FWD
         self.calls = {"allgather": 0, "reducescatter": 0}
+        # the reference's per-step communication ledger (sharded.py:115-181)
+        self.ledger = CommLedger()
+        self.entry = LedgerEntry(step=0)
 
     def forward(self):
         self.phase = PHASE_W_FWD
@@ -58,8 +61,11 @@ class QSDPContext:
     def backward(self):
         self.phase = PHASE_W_BWD
 
-    def next_step(self):
+    def next_step(self, step_time_s: float = 0.0):
+        self.entry.step_time_s = step_time_s
+        self.ledger.append(self.entry)
         self.step += 1
+        self.entry = LedgerEntry(step=self.step)
         self.phase = PHASE_W_FWD
 
     def close(self):
@@ -85,6 +91,7 @@ class QSDPAllGather(AllGather):
         c = self.ctx
         c.ag.all_gather(input_tensor, segs, SegmentKey(c.root_seed, c.step, self.layer, c.phase, 0), output_tensor)
         c.calls["allgather"] += 1
+        record_allgather(c.entry, f"group{self.layer}", segs, c.wspec)
         return None
 
 
@@ -110,6 +117,7 @@ class QSDPReduceScatter(ReduceScatter):
         c.rs.reduce_scatter(input_tensor, segs, SegmentKey(c.root_seed, c.step, self.layer, PHASE_GRAD, c.rank),
                             output_tensor)
         c.calls["reducescatter"] += 1
+        record_reducescatter(c.entry, f"group{self.layer}", segs, c.gspec)
         return None
 
 

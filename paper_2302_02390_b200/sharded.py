@@ -4,7 +4,8 @@ Mirrors pkg/src/qsdp/sharded.py of the reference:
 
 * constants ``PHASE_W_FWD/PHASE_W_BWD/PHASE_GRAD`` (sharded.py:56-58),
   ``QuantConfig`` (:76-93), ``shard_bounds`` (:193-200), ``Transfer`` /
-  ``LedgerEntry`` (:115-158) with identical accounting;
+  ``LedgerEntry`` (:115-158) with identical accounting and ``CommLedger``
+  (:161-181) with a byte-identical CSV export;
 * :class:`QSDPHooks` -- ``_gather(step, layer_idx, phase, entry)`` and
   ``_reduce_scatter(step, layer_idx, per_worker_grads, entry)`` with the exact
   signatures, semantics, keys and ledger records of ``ShardedMLP._gather``
@@ -28,7 +29,7 @@ from .quantize import QuantSpec, SegmentKey, dequant_accumulate, dequantize_segm
     message_size_bits, quantize_segments
 
 __all__ = ["PHASE_W_FWD", "PHASE_W_BWD", "PHASE_GRAD", "QuantConfig", "LayerSpec", "Transfer",
-           "LedgerEntry", "shard_bounds", "QSDPHooks", "gather_segments", "reduce_scatter_segments"]
+           "LedgerEntry", "CommLedger", "shard_bounds", "QSDPHooks", "gather_segments", "reduce_scatter_segments"]
 
 PHASE_W_FWD = 0
 PHASE_W_BWD = 1
@@ -120,6 +121,27 @@ class LedgerEntry:
         else:
             self.reducescatter_bits += t.total_bits
             self.reducescatter_payload_bits += t.payload_bits * t.copies
+
+
+class CommLedger:
+    """Per-step communication record with CSV export (sharded.py:161-181)."""
+
+    def __init__(self):
+        self.entries: list = []
+
+    def append(self, entry: LedgerEntry) -> None:
+        self.entries.append(entry)
+
+    def to_csv(self, path, no_timestamp: bool = True) -> None:
+        import csv
+        with open(path, "w", newline="") as fh:
+            if not no_timestamp:
+                import datetime
+                fh.write(f"# generated {datetime.datetime.now().isoformat()}\n")
+            w = csv.writer(fh)
+            w.writerow(["step", "allgather_bits", "reducescatter_bits", "step_time_s"])
+            for e in self.entries:
+                w.writerow([e.step, e.allgather_bits, e.reducescatter_bits, repr(e.step_time_s)])
 
 
 def shard_bounds(size: int, P: int):

@@ -15,6 +15,9 @@ reference functions:
             uniform, learned, out-of-[0,1] and 2^12 / 2^16-level tables;
 * ll_*:     learn_levels(values, table, lr) outputs (quantize.py:366-397),
             including the re-sort / collision-nudge and distinct-count paths;
+* wire_*:   malformed / edge-case messages and the exception class (or "ok") the
+            reference decode() raises for each (wire.py:134-184);
+* ledger_csv: CommLedger.to_csv bytes of a ShardedMLP run (sharded.py:161-181);
 * hook_*:   inputs/outputs of ShardedMLP._gather / ._reduce_scatter recorded
             during a short ShardedMLP run (sharded.py:323-433), plus the run's
             ledger bits and losses, and ReferenceMLP's final parameters.
@@ -158,6 +161,47 @@ def _levels(out):
     out["ll_lr"] = np.array(lrows)
 
 
+def _wire_cases(out):
+    from qsdp.quantize import QuantizedBlock
+    from qsdp.wire import decode
+    import struct
+    rng = np.random.default_rng(611)
+
+    def blk(codes, bits, shift=0.0, lo=0.0, hi=1.0):
+        c = np.asarray(codes, dtype=np.uint32)
+        return QuantizedBlock(codes=c, shift=shift, scale_lo=lo, scale_hi=hi, bit_width=bits, length=c.size)
+
+    base = encode([blk(rng.integers(0, 8, 5), 3), blk(rng.integers(0, 8, 5), 3), blk(rng.integers(0, 8, 3), 3)])
+    two = encode([blk(np.arange(4), 4), blk(np.arange(4), 4)])
+    msgs = [b"", b"\x01\x02", base, base[:13], base[:14], base[:20], base[:14 + 12], base[:14 + 13 + 1],
+            base[:-1], base + b"\x00", base + b"\x00\x00\x07"]
+    m = bytearray(base); m[0] = 9; msgs.append(bytes(m))
+    m = bytearray(base); m[1] = 0; msgs.append(bytes(m))
+    m = bytearray(base); m[1] = 40; msgs.append(bytes(m))
+    m = bytearray(base); m[1] = 17; msgs.append(bytes(m))
+    m = bytearray(two); m[10:14] = (99).to_bytes(4, "little"); msgs.append(bytes(m))
+    m = bytearray(two); m[2:6] = (0).to_bytes(4, "little"); msgs.append(bytes(m))
+    m = bytearray(base); m[14 + 12 + 1] ^= 0x80; msgs.append(bytes(m))            # padding bit of block 0
+    m = bytearray(base); m[-1] ^= 0x40; msgs.append(bytes(m))                     # padding of the last block
+    m = bytearray(base); m[14 + 4:14 + 8] = struct.pack("<f", 5.0); msgs.append(bytes(m))  # lo > hi, block 0
+    m = bytearray(base); m[14 + 14 + 4:14 + 14 + 8] = struct.pack("<f", float("nan")); msgs.append(bytes(m))
+    m = bytearray(base); m[14 + 14 + 4:14 + 14 + 8] = struct.pack("<f", 5.0); m[-1] ^= 0x40; msgs.append(bytes(m))
+    m = bytearray(base); m[-1] ^= 0x40; msgs.append(bytes(m[:-2]))               # padding + truncation later
+    m = bytearray(base); m[14 + 12 + 1] ^= 0x80; msgs.append(bytes(m[:-1]))      # padding at 0, truncated at 2
+    msgs.append(bytes([1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0]))                  # canonical empty
+    msgs.append(bytes([1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 5, 0, 0, 0]))                  # empty with total 5
+    msgs.append(bytes([1, 3, 5, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0]) + b"\x00")       # empty + trailing
+    for i, msg in enumerate(msgs):
+        try:
+            decode(msg)
+            res = "ok"
+        except Exception as e:  # noqa: BLE001 - record the class
+            res = type(e).__name__
+        out[f"wire_{i}_msg"] = np.frombuffer(msg, dtype=np.uint8) if msg else np.zeros(0, dtype=np.uint8)
+        out[f"wire_{i}_res"] = np.array(res)
+    out["wire_n"] = np.array(len(msgs))
+
+
 def main():
     rng = np.random.default_rng(7)
     out = {"numpy_version": np.array(np.__version__)}
@@ -228,6 +272,13 @@ def main():
             losses.append(loss)
             bits_ag.append(entry.allgather_bits)
             bits_rs.append(entry.reducescatter_bits)
+        if not hook_rows:
+            import tempfile
+            with tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False) as fh:
+                path = fh.name
+            sim.ledger.to_csv(path)
+            out["ledger_csv"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+            os.unlink(path)
         ref = ReferenceMLP(cfg)
         ref_losses = ref.run(2)
         assert ref_losses == losses
@@ -250,6 +301,7 @@ def main():
         hook_rows.append(run_id)
     out["n_hooks"] = np.array(hook_idx)
     _levels(out)
+    _wire_cases(out)
     out["n_runs"] = np.array(len(hook_rows))
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {os.path.getsize(OUT)/1e6:.2f} MB, {len(cases)} quant cases, "

@@ -82,3 +82,36 @@ def test_invalid_config_is_value_error_without_gpu():
     assert st == _lib.QSDP_EINVAL
     with pytest.raises(ValueError, match="bit_width"):
         _lib.check(st)
+
+
+def test_ledger_csv_matches_reference_bytes(golden, tmp_path):
+    """CommLedger.to_csv is byte-identical to the reference's (sharded.py:161-181)."""
+    from paper_2302_02390_b200.sharded import CommLedger, LedgerEntry
+    bits = golden["run_0_bits"]
+    led = CommLedger()
+    for t in range(bits.shape[1]):
+        led.append(LedgerEntry(step=t, allgather_bits=int(bits[0, t]), reducescatter_bits=int(bits[1, t])))
+    path = tmp_path / "ledger.csv"
+    led.to_csv(path)
+    assert path.read_bytes() == bytes(golden["ledger_csv"])
+
+
+def test_collective_ledger_records(oracle):
+    """record_allgather / record_reducescatter charge the reference's message sizes
+    (sharded.py:349-358, 403-413) for any segmentation."""
+    from paper_2302_02390_b200.comm import record_allgather, record_reducescatter
+    from paper_2302_02390_b200.quantize import QuantSpec
+    from paper_2302_02390_b200.sharded import LedgerEntry
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        P = int(rng.integers(1, 9))
+        segs = [(0, int(n)) for n in rng.integers(0, 5000, P)]
+        spec = QuantSpec(int(rng.integers(1, 17)), int(rng.integers(1, 2000)), "shift")
+        e = LedgerEntry(step=0)
+        record_allgather(e, "w", segs, spec)
+        record_reducescatter(e, "w", segs, spec)
+        msg = [oracle.message_size_bits(n, spec.bucket, spec.bits) if n else 0 for _, n in segs]
+        assert e.allgather_bits == sum(m * (P - 1) for m in msg)
+        assert e.reducescatter_bits == sum(m * (P - 1) for m in msg)
+        assert e.allgather_payload_bits == sum(n * spec.bits * (P - 1) for _, n in segs)
+        assert e.allgather_events == e.reducescatter_events == 1
