@@ -428,6 +428,52 @@ def main():
                             "frac_of_hbm_peak": round(lbytes[name] / (tk * 1e-3) / 1e9 / hbm_peak, 4),
                             "bytes_per_pass": lbytes[name], "launches_per_pass": len(state)}
 
+    # ---- GPU wire codec over the step's weight messages (world 1) ----
+    wire = None
+    if world == 1 and not args.no_levels:
+        from paper_2302_02390_b200.wire import decode_segment, encode_segment
+        for gi, st in enumerate(state):  # fill the weight slots with real codes first
+            quantize_segments([(st["shard"], 0, SegmentKey(0, 0, gi, 0, 0))], wspec, out=[st["wq"]])
+        msgs = [encode_segment(st["wq"][0], st["wq"][1], st["g"].numel, wspec) for st in state]
+        mbytes = sum(m.numel() for m in msgs)
+
+        def enc_all():
+            for st, m in zip(state, msgs):
+                encode_segment(st["wq"][0], st["wq"][1], st["g"].numel, wspec, out=m)
+
+        wire = {"messages": len(msgs), "message_bytes": mbytes}
+        gk = capture(enc_all)
+        gk.replay()
+        torch.cuda.synchronize(dev)
+        evk = time_graph(gk, args.steps)
+        torch.cuda.synchronize(dev)
+        tk = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+        wire["encode"] = {"ms_per_pass": round(tk, 4), "gbs": round(2 * mbytes / (tk * 1e-3) / 1e9, 1),
+                          "bytes_per_pass": 2 * mbytes}
+        for m in msgs:  # warm the decode path (module load, allocator)
+            decode_segment(m)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.fill_(7)
+        a.record(stream)
+        for m in msgs:  # decode = header parse (14-byte D2H) + one kernel + error check per message
+            decode_segment(m)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        td = a.elapsed_time(b)
+        wire["decode_incl_host_checks"] = {"ms_per_pass": round(td, 4), "gbs": round(2 * mbytes / (td * 1e-3) / 1e9, 1)}
+        # the decode kernel alone (headers parsed once; the per-message host checks excluded)
+        from paper_2302_02390_b200.wire import decode_kernels
+        dk = decode_kernels(msgs)
+        gk = capture(dk)
+        gk.replay()
+        torch.cuda.synchronize(dev)
+        evk = time_graph(gk, args.steps)
+        torch.cuda.synchronize(dev)
+        tk = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+        wire["decode"] = {"ms_per_pass": round(tk, 4), "gbs": round(2 * mbytes / (tk * 1e-3) / 1e9, 1),
+                          "bytes_per_pass": 2 * mbytes}
+
     # ---- e2e: through the C-ABI communicator, host buffers, copies inside the timed region ----
     e2e = None
     if not args.no_e2e:
@@ -509,7 +555,7 @@ def main():
                                     + ("fused single-launch collectives" if comm_fused else "3 launches per collective"),
                        "convention": "sum over ranks of 4*N per collective / time"},
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
-            "levels": levels,
+            "levels": levels, "wire": wire,
             "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

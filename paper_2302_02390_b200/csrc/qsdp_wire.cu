@@ -7,9 +7,10 @@
 //   block j <fff    shift, scale_lo, scale_hi                        12 bytes
 //           payload ceil(len_j * bits / 8) bytes, LSB-first, zero-padded
 //
-// Both directions are gathers: one thread produces 16 consecutive output bytes
-// (vector store when aligned), locating its block once and walking forward, so
-// the codec is a single HBM-bound pass (read c, write c bytes per element).
+// Both directions run one warp per block; the payload copy writes aligned 4-byte
+// destination words assembled from aligned source words with funnel shifts (the
+// message puts payloads at offsets = 2 mod 4), so the codec is a single
+// HBM-bound pass (read c, write c bytes per element).
 // Decode also validates every complete block: nonzero padding bits
 // (DecodeError, wire.py:90-91) and scale_lo <= scale_hi (QuantizedBlock,
 // quantize.py:109-110), reporting the first failing block per kind.
@@ -22,98 +23,82 @@
 namespace qsdp {
 
 
-// byte o (>= 14) of the message: block j, offset w inside the block's wire bytes
-__device__ __forceinline__ uint8_t wire_byte_at(const uint8_t* __restrict__ codes, const uint8_t* __restrict__ meta,
-                                                const WireGeom& g, int64_t j, int64_t w) {
-  if (w < 12) return meta[12 * j + w];
-  return codes[j * g.pbs + (w - 12)];
+// Warp-cooperative copy of n bytes between arbitrarily aligned buffers: single
+// bytes up to an 8-aligned destination, then whole 8-byte destination words
+// assembled from two aligned source words (64-bit funnel shift; 4 words in
+// flight per lane), then the tail bytes.
+__device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int64_t n,
+                                          int lane) {
+  int64_t h = (8 - ((uintptr_t)dst & 7)) & 7;
+  if (h > n) h = n;
+  if (lane < h) dst[lane] = src[lane];
+  const int64_t nw = (n - h) >> 3;  // whole destination words
+  const uint8_t* s0 = src + h;
+  const int sh = (int)((uintptr_t)s0 & 7);
+  const unsigned long long* sa = reinterpret_cast<const unsigned long long*>(s0 - sh);
+  unsigned long long* dw = reinterpret_cast<unsigned long long*>(dst + h);
+  // with sh != 0 the last word read, sa[nw], is the word holding the last body
+  // byte (s0 + 8*nw - 1), so no read leaves the source span's words
+  constexpr int U = 4;
+  for (int64_t i0 = lane; i0 < nw; i0 += 32 * U) {
+    unsigned long long lo[U], hi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + 32 * u;
+      lo[u] = i < nw ? sa[i] : 0ull;
+      hi[u] = (sh && i < nw) ? sa[i + 1] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + 32 * u;
+      if (i < nw) dw[i] = sh ? (lo[u] >> (8 * sh)) | (hi[u] << (64 - 8 * sh)) : lo[u];
+    }
+  }
+  for (int64_t k = h + 8 * nw + lane; k < n; k += 32) dst[k] = src[k];
 }
 
+// One warp per block: the block's 12 meta bytes and payload go to their message
+// offsets (14 + j*blk); block 0's warp also writes the 14 header bytes.
 __global__ void __launch_bounds__(256) wire_encode_kernel(const uint8_t* __restrict__ codes,
                                                           const float* __restrict__ meta,
                                                           const __grid_constant__ WireGeom g, uint8_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint8_t* mb = reinterpret_cast<const uint8_t*>(meta);
-  const int64_t nchunk = (g.msg_bytes + 15) / 16;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunk; c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o0 = 16 * c;
-    uint8_t buf[16];
-    // locate the block of the first body byte of the chunk once, then walk
-    int64_t j = 0, w = 0;
-    if (o0 >= 14) {
-      j = (o0 - 14) / g.blk;
-      w = (o0 - 14) - j * g.blk;
-    }
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int64_t o = o0 + k;
-      uint8_t v = 0;
-      if (o < 14) {
-        v = g.header[o];
-      } else if (o < g.msg_bytes) {
-        v = wire_byte_at(codes, mb, g, j, w);
-        if (++w == g.blk) {
-          w = 0;
-          ++j;
-        }
-      }
-      buf[k] = v;
-    }
-    uint8_t* dst = out + o0;
-    if (o0 + 16 <= g.msg_bytes && ((uintptr_t)dst & 15) == 0) {
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(buf);
-    } else {
-      for (int k = 0; k < 16 && o0 + k < g.msg_bytes; ++k) dst[k] = buf[k];
-    }
+  if (warp == 0 && lane < 14) out[lane] = g.header[lane];
+  for (int64_t j = warp; j < g.nb; j += nwarps) {
+    uint8_t* d = out + 14 + j * g.blk;
+    if (lane < 12) d[lane] = mb[12 * j + lane];
+    warp_copy(d + 12, codes + j * g.pbs, j == g.nb - 1 ? g.last_pb : g.pbs, lane);
   }
 }
 
-// Decode the first `nblk` (complete) blocks: codes chunks are gathered from the
-// payloads, meta from the block headers; err[0] = first block with nonzero
-// padding bits, err[1] = first block with !(lo <= hi) (atomicMin; init INT64_MAX).
+// Decode the first `nblk` (complete) blocks, one warp per block: payload to the
+// packed layout, meta to float[nb][3]; err[0] = first block with nonzero padding
+// bits, err[1] = first block with !(lo <= hi) (atomicMin; init UINT64_MAX).
 __global__ void __launch_bounds__(256) wire_decode_kernel(const uint8_t* __restrict__ msg, const __grid_constant__ WireGeom g,
                                                           int64_t nblk, uint8_t* __restrict__ codes,
                                                           float* __restrict__ meta, unsigned long long* err) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  const int64_t cbytes = nblk == g.nb ? g.codes_bytes : nblk * g.pbs;
-  const int64_t nchunk = (cbytes + 15) / 16;
-  for (int64_t c = tid; c < nchunk; c += nth) {
-    const int64_t c0 = 16 * c;
-    int64_t j = c0 / g.pbs, w = c0 - j * g.pbs;
-    uint8_t buf[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      uint8_t v = 0;
-      if (c0 + k < cbytes) {
-        v = msg[14 + j * g.blk + 12 + w];
-        if (++w == g.pbs) {
-          w = 0;
-          ++j;
-        }
-      }
-      buf[k] = v;
-    }
-    uint8_t* dst = codes + c0;
-    if (c0 + 16 <= cbytes && ((uintptr_t)dst & 15) == 0) {
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(buf);
-    } else {
-      for (int k = 0; k < 16 && c0 + k < cbytes; ++k) dst[k] = buf[k];
-    }
-  }
-  // per block: meta + validation
-  for (int64_t j = tid; j < nblk; j += nth) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = warp; j < nblk; j += nwarps) {
     const uint8_t* h = msg + 14 + j * g.blk;
-    float m[3];
-    uint8_t* mb = reinterpret_cast<uint8_t*>(m);
-    for (int k = 0; k < 12; ++k) mb[k] = h[k];
-    meta[3 * j] = m[0];
-    meta[3 * j + 1] = m[1];
-    meta[3 * j + 2] = m[2];
     const int64_t n = j == g.nb - 1 ? g.last_n : (int64_t)g.bucket;
     const int64_t pb = j == g.nb - 1 ? g.last_pb : g.pbs;
-    const int used = (int)((n * g.bits) & 7);
-    if (used != 0 && (h[12 + pb - 1] >> used) != 0) atomicMin(&err[0], (unsigned long long)j);
-    if (!(m[1] <= m[2])) atomicMin(&err[1], (unsigned long long)j);
+    warp_copy(codes + j * g.pbs, h + 12, pb, lane);
+    if (lane == 0) {
+      float m[3];
+      uint8_t* mbytes = reinterpret_cast<uint8_t*>(m);
+      for (int k = 0; k < 12; ++k) mbytes[k] = h[k];
+      meta[3 * j] = m[0];
+      meta[3 * j + 1] = m[1];
+      meta[3 * j + 2] = m[2];
+      const int used = (int)((n * g.bits) & 7);
+      if (used != 0 && (h[12 + pb - 1] >> used) != 0) atomicMin(&err[0], (unsigned long long)j);
+      if (!(m[1] <= m[2])) atomicMin(&err[1], (unsigned long long)j);
+    }
   }
 }
 
@@ -160,16 +145,23 @@ static int grid_for_bytes(int64_t bytes, int sms) {
   return (int)(blocks < 1 ? 1 : blocks);
 }
 
+static int grid_for_blocks(int64_t nb, int sms) {
+  int64_t blocks = (nb + 7) / 8;  // 8 warps per CTA, one warp per block
+  const int64_t cap = (int64_t)sms * 8;
+  if (blocks > cap) blocks = cap;
+  return (int)(blocks < 1 ? 1 : blocks);
+}
+
 cudaError_t launch_wire_encode(const uint8_t* codes, const float* meta, const WireGeom& g, uint8_t* out, int sms,
                                cudaStream_t s) {
-  wire_encode_kernel<<<grid_for_bytes(g.msg_bytes, sms), 256, 0, s>>>(codes, meta, g, out);
+  wire_encode_kernel<<<grid_for_blocks(g.nb, sms), 256, 0, s>>>(codes, meta, g, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_wire_decode(const uint8_t* msg, const WireGeom& g, int64_t nblk, uint8_t* codes, float* meta,
                                unsigned long long* err, int sms, cudaStream_t s) {
   if (nblk <= 0) return cudaSuccess;
-  wire_decode_kernel<<<grid_for_bytes(nblk * g.blk, sms), 256, 0, s>>>(msg, g, nblk, codes, meta, err);
+  wire_decode_kernel<<<grid_for_blocks(nblk, sms), 256, 0, s>>>(msg, g, nblk, codes, meta, err);
   return cudaGetLastError();
 }
 

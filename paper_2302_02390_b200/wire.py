@@ -151,6 +151,28 @@ def decode_segment(msg: torch.Tensor) -> DecodedSegment:
     return DecodedSegment(codes[: _codes_bytes(L, bits, bucket)], meta[:nb], L, bits, bucket)
 
 
+def decode_kernels(msgs):
+    """A callable launching only the decode kernels of well-formed ``msgs``
+    (headers parsed once up front): for timing / CUDA-graph capture."""
+    jobs = []
+    for m in msgs:
+        n = m.numel()
+        hdr = m[:14].cpu().numpy()
+        info = _lib.WireInfo()
+        _lib.check(_lib.lib().qsdp_wire_parse(hdr.ctypes.data, n, ctypes.byref(info)))
+        L, bits, bucket = int(info.total_length), int(info.bits), int(info.bucket)
+        codes = torch.empty(max(_codes_bytes(L, bits, bucket), 1), dtype=torch.uint8, device=m.device)
+        meta = torch.empty((max(-(-L // bucket), 1), 3), dtype=torch.float32, device=m.device)
+        err = torch.full((2,), -1, dtype=torch.int64, device=m.device)
+        jobs.append((m, info, codes, meta, err))
+
+    def run():
+        for m, info, codes, meta, err in jobs:
+            _lib.check(_lib.lib().qsdp_wire_decode_device(m.data_ptr(), ctypes.byref(info), codes.data_ptr(),
+                                                          meta.data_ptr(), err.data_ptr(), _stream(m.device)))
+    return run
+
+
 # ---------------------------------------------------------------------------
 # The reference's host-object API (blocks in host memory), on the device codec.
 # ---------------------------------------------------------------------------
