@@ -24,6 +24,8 @@
  *   decode  wire.py:134-184                            qsdp_wire_parse + qsdp_wire_decode_device
  *   ShardedMLP._gather  sharded.py:323-373             qsdp_all_gather (one process per GPU)
  *   ShardedMLP._reduce_scatter  sharded.py:375-433     qsdp_reduce_scatter
+ *   qsdp_step (lattice projection)  optimizer.py:194-229  qsdp_reduce_scatter_lattice /
+ *                                                        qsdp_dequant_accumulate_lattice (K4 epilogue)
  *   quantize_bucket (levels) + quantize_with_levels    qsdp_quantize_levels / _batch
  *     quantize.py:235-286, 400-416                       (inner = QSDP_INNER_LEVELS)
  *   dequantize(block, "levels", table)  quantize.py:225-231  qsdp_dequantize_levels / _batch
@@ -213,6 +215,20 @@ qsdp_status qsdp_pack_codes(const uint32_t* codes, int64_t length, const qsdp_qc
 qsdp_status qsdp_unpack_codes(const uint8_t* packed, int64_t length, const qsdp_qcfg* cfg, uint32_t* codes,
                               void* stream);
 
+/* ---- lattice-projected step fused with the reduce-scatter epilogue ----
+ * With g = the K4 average (fp64, before any rounding): x <- d*rint((x - c*g - r)/d) + r
+ * (qsdp_step, optimizer.py:212-216), r = sample_shift(d, bucket_rng(shift_key..., 0)), the
+ * first draw of the keyed stream (its step also advances with the comm's device step). */
+typedef struct {
+  double lr_over_beta;  /* c = eta / beta */
+  double delta;         /* d: fine lattice pitch (> 0) */
+  qsdp_key shift_key;
+  int32_t x_dtype;      /* QSDP_F32 | QSDP_F64 (fp64 iterates are bit-exact with the reference) */
+} qsdp_lattice;
+qsdp_status qsdp_dequant_accumulate_lattice(const uint8_t* const* codes, const float* const* meta, int32_t nsrc,
+                                            int64_t length, const qsdp_qcfg* cfg, int32_t divisor, void* g_out,
+                                            int32_t out_dtype, void* x, const qsdp_lattice* lat, void* stream);
+
 /* ---- host wire export (wire.py:108-131): codes/meta already on the host ---- */
 int64_t qsdp_wire_encode(const uint8_t* codes, const float* meta, int64_t length,
                          const qsdp_qcfg* cfg, uint8_t* out, int64_t out_cap);
@@ -248,6 +264,11 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype,
 qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_dtype,
                                 const qsdp_segment* segs, const qsdp_key* key, void* shard_out,
                                 int32_t out_dtype, void* stream);
+/* C2 with the lattice step on the owner's shard: shard_out (may be NULL) receives the
+ * average gradient, x_shard (lat->x_dtype) the projected iterate.  Never fused. */
+qsdp_status qsdp_reduce_scatter_lattice(qsdp_comm* c, const void* full_grad, int32_t in_dtype,
+                                        const qsdp_segment* segs, const qsdp_key* key, void* shard_out,
+                                        int32_t out_dtype, void* x_shard, const qsdp_lattice* lat, void* stream);
 qsdp_status qsdp_comm_destroy(qsdp_comm* c);
 
 #ifdef __cplusplus

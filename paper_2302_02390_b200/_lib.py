@@ -42,7 +42,7 @@ EXPORTED_SYMBOLS = (
     "qsdp_quantize_levels", "qsdp_quantize_levels_batch", "qsdp_dequantize_levels",
     "qsdp_dequantize_levels_batch", "qsdp_learn_levels", "qsdp_comm_set_weight_levels",
     "qsdp_wire_parse", "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes",
-    "qsdp_unpack_codes",
+    "qsdp_unpack_codes", "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice",
 )
 
 
@@ -69,6 +69,11 @@ class QItem(ctypes.Structure):
 class DItem(ctypes.Structure):
     _fields_ = [("codes", ctypes.c_void_p * 8), ("meta", ctypes.c_void_p * 8),
                 ("nsrc", ctypes.c_int32), ("length", ctypes.c_int64), ("out", ctypes.c_void_p)]
+
+
+class Lattice(ctypes.Structure):
+    _fields_ = [("lr_over_beta", ctypes.c_double), ("delta", ctypes.c_double), ("shift_key", Key),
+                ("x_dtype", ctypes.c_int32)]
 
 
 class WireInfo(ctypes.Structure):
@@ -149,6 +154,9 @@ def lib():
     L.qsdp_wire_encode_device.argtypes = [vp, vp, i64, cfgp, vp, i64, vp]
     L.qsdp_wire_decode_device.argtypes = [vp, ctypes.POINTER(WireInfo), vp, vp, vp, vp]
     L.qsdp_pack_codes.argtypes = [vp, i64, cfgp, vp, vp]
+    L.qsdp_dequant_accumulate_lattice.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i64, cfgp, i32, vp,
+                                                  i32, vp, ctypes.POINTER(Lattice), vp]
+    L.qsdp_reduce_scatter_lattice.argtypes = [vp, vp, i32, segp, keyp, vp, i32, vp, ctypes.POINTER(Lattice), vp]
     L.qsdp_unpack_codes.argtypes = [vp, i64, cfgp, vp, vp]
     L.qsdp_dequantize.argtypes = [vp, vp, i64, cfgp, vp, i32, vp]
     L.qsdp_dequantize_batch.argtypes = [ctypes.POINTER(DItem), i32, cfgp, i32, vp]
@@ -175,7 +183,8 @@ def lib():
                  "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_levels",
                  "qsdp_quantize_levels_batch", "qsdp_dequantize_levels", "qsdp_dequantize_levels_batch",
                  "qsdp_learn_levels", "qsdp_comm_set_weight_levels", "qsdp_wire_parse",
-                 "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes", "qsdp_unpack_codes"):
+                 "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes", "qsdp_unpack_codes",
+                 "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib

@@ -204,6 +204,24 @@ class QSDPComm:
                 _DTYPE_CODE[out.dtype], torch.cuda.current_stream(self.device).cuda_stream))
         return out
 
+    def reduce_scatter_lattice(self, full_grad: torch.Tensor, segs, key: SegmentKey, x_shard: torch.Tensor,
+                               step, out: torch.Tensor | None = None) -> torch.Tensor:
+        """C2 + the lattice-projected step on this rank's shard, in the K4 epilogue
+        (``step`` a :class:`~.lattice.LatticeStep`): ``x_shard``
+        moves in place; ``out`` (optional) receives the average gradient."""
+        if x_shard.numel() < segs[self.rank][1]:
+            raise ValueError("iterate shorter than this rank's segment")
+        arr = self._segs(segs)
+        k = key.c()
+        lat = step.c(x_shard.dtype)
+        odt = out.dtype if out is not None else torch.float32
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().qsdp_reduce_scatter_lattice(
+                self._h, full_grad.data_ptr(), _DTYPE_CODE[full_grad.dtype], arr, ctypes.byref(k),
+                out.data_ptr() if out is not None else None, _DTYPE_CODE[odt], x_shard.data_ptr(), ctypes.byref(lat),
+                torch.cuda.current_stream(self.device).cuda_stream))
+        return x_shard
+
     def reduce_scatter(self, full_grad: torch.Tensor, segs, key: SegmentKey, out: torch.Tensor) -> torch.Tensor:
         """C2: ``out`` (this rank's shard) receives the fp64-ordered average of
         every rank's dequantized contribution to segs[rank]."""

@@ -16,6 +16,7 @@
 // the barrier of call k+1, i.e. finished reading call k-1's data.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -206,10 +207,11 @@ struct DJobSpec {
   int nsrc;
   int64_t length;
   void* out;
+  void* lat_x = nullptr;  // lattice step iterate (K4 epilogue)
 };
 
 void build_dtab(DJobTable& tab, const std::vector<DJobSpec>& jobs, size_t& i, const qsdp_qcfg* cfg, int accumulate,
-                int divisor, int out_dtype, const DynSrc& dyn, bool& vec) {
+                int divisor, int out_dtype, const DynSrc& dyn, bool& vec, const qsdp_lattice* lat = nullptr) {
   memset(&tab, 0, sizeof(tab));
   tab.bits = cfg->bits;
   tab.bucket = cfg->bucket;
@@ -234,6 +236,7 @@ void build_dtab(DJobTable& tab, const std::vector<DJobSpec>& jobs, size_t& i, co
     }
     J.nsrc = s.nsrc;
     J.out = s.out;
+    J.lat_x = s.lat_x;
     J.length = s.length;
     J.bucket_base = nb;
     nb += (s.length + cfg->bucket - 1) / cfg->bucket;
@@ -242,11 +245,23 @@ void build_dtab(DJobTable& tab, const std::vector<DJobSpec>& jobs, size_t& i, co
   tab.njobs = nj;
   tab.total_buckets = nb;
   tab.codes_vec = cvec ? 1 : 0;
+  if (lat != nullptr) {
+    tab.lat_on = 1;
+    tab.lat_xdtype = lat->x_dtype == QSDP_F64 ? 1 : 0;
+    tab.lat_c = lat->lr_over_beta;
+    tab.lat_d = lat->delta;
+    tab.lat_key[0] = lat->shift_key.root_seed;
+    tab.lat_key[1] = lat->shift_key.step;
+    tab.lat_key[2] = lat->shift_key.layer;
+    tab.lat_key[3] = lat->shift_key.phase;
+    tab.lat_key[4] = lat->shift_key.worker;
+    tab.lat_step_ptr = dyn.step_ptr;
+  }
 }
 
 qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg, int accumulate,
                         int divisor, int out_dtype, cudaStream_t stream, const DynSrc& dyn = DynSrc(),
-                        const double* levels = nullptr) {
+                        const double* levels = nullptr, const qsdp_lattice* lat = nullptr) {
   if (out_dtype != QSDP_F32 && out_dtype != QSDP_F64 && out_dtype != QSDP_BF16)
     return fail(QSDP_EINVAL, "output dtype must be f32, f64 or bf16");
   int sms = 0;
@@ -258,7 +273,7 @@ qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg,
   while (i < jobs.size()) {
     DJobTable tab;
     bool vec = false;
-    build_dtab(tab, jobs, i, cfg, accumulate, divisor, out_dtype, dyn, vec);
+    build_dtab(tab, jobs, i, cfg, accumulate, divisor, out_dtype, dyn, vec, lat);
     if (tab.njobs == 0) continue;
     bool out16 = true;  // 16-byte vector stores of the levels fast path (bf16 included)
     for (int k = 0; k < tab.njobs; ++k) out16 = out16 && aligned(tab.jobs[k].out, 16);
@@ -483,6 +498,35 @@ qsdp_status qsdp_dequant_accumulate(const uint8_t* const* codes, const float* co
 qsdp_status qsdp_dequant_accumulate_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
                                           int32_t divisor, int32_t out_dtype, void* stream) {
   return dequant_items(items, nitems, cfg, 1, divisor, out_dtype, stream);
+}
+
+static qsdp_status check_lattice(const qsdp_lattice* lat, const void* x) {
+  if (lat == nullptr || x == nullptr) return fail(QSDP_EINVAL, "null lattice argument");
+  if (!(lat->delta > 0) || !std::isfinite(lat->delta)) return fail(QSDP_EINVAL, "resolution must be > 0");
+  if (!std::isfinite(lat->lr_over_beta)) return fail(QSDP_EINVAL, "step size must be finite");
+  if (lat->x_dtype != QSDP_F32 && lat->x_dtype != QSDP_F64) return fail(QSDP_EINVAL, "iterate dtype must be f32 or f64");
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_dequant_accumulate_lattice(const uint8_t* const* codes, const float* const* meta, int32_t nsrc,
+                                            int64_t length, const qsdp_qcfg* cfg, int32_t divisor, void* g_out,
+                                            int32_t out_dtype, void* x, const qsdp_lattice* lat, void* stream) {
+  qsdp_status st = check_lattice(lat, x);
+  if (st != QSDP_OK) return st;
+  st = check_cfg(cfg);
+  if (st != QSDP_OK) return st;
+  if (nsrc < 1 || nsrc > 8) return fail(QSDP_EINVAL, "nsrc must be in [1, 8]");
+  std::vector<DJobSpec> jobs(1);
+  memset(&jobs[0], 0, sizeof(DJobSpec));
+  for (int p = 0; p < nsrc; ++p) {
+    jobs[0].codes[p] = codes[p];
+    jobs[0].meta[p] = meta[p];
+  }
+  jobs[0].nsrc = nsrc;
+  jobs[0].length = length;
+  jobs[0].out = g_out;
+  jobs[0].lat_x = x;
+  return run_dequant(jobs, cfg, 1, divisor, out_dtype, reinterpret_cast<cudaStream_t>(stream), DynSrc(), nullptr, lat);
 }
 
 static void put_u32_le(uint8_t* p, uint32_t v) { memcpy(p, &v, 4); }
@@ -974,8 +1018,19 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
   return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0), lv ? c->wlevels : nullptr);
 }
 
+static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int32_t in_dtype,
+                                       const qsdp_segment* segs, const qsdp_key* key, void* shard_out,
+                                       int32_t out_dtype, void* stream, void* x_shard, const qsdp_lattice* lat);
+
 qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_dtype, const qsdp_segment* segs,
                                 const qsdp_key* key, void* shard_out, int32_t out_dtype, void* stream) {
+  if (shard_out == nullptr) return fail(QSDP_EINVAL, "null output");
+  return reduce_scatter_impl(c, full_grad, in_dtype, segs, key, shard_out, out_dtype, stream, nullptr, nullptr);
+}
+
+static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int32_t in_dtype,
+                                       const qsdp_segment* segs, const qsdp_key* key, void* shard_out,
+                                       int32_t out_dtype, void* stream, void* x_shard, const qsdp_lattice* lat) {
   if (c == nullptr || key == nullptr) return fail(QSDP_EINVAL, "null argument");
   qsdp_status st = check_segs(c, segs);
   if (st != QSDP_OK) return st;
@@ -1004,7 +1059,8 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
   d[0].nsrc = c->world;
   d[0].length = segs[c->rank].length;
   d[0].out = shard_out;
-  if (fused_cfg_ok(c, cfg, in_dtype)) {
+  d[0].lat_x = x_shard;
+  if (lat == nullptr && fused_cfg_ok(c, cfg, in_dtype)) {
     bool launched = false;
     st = try_fused(c, q, d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 1), launched);
     if (st != QSDP_OK || launched) return st;
@@ -1016,7 +1072,15 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
     if (st != QSDP_OK) return st;
   }
   // 3. owner dequant-accumulates sources 0..P-1 (in order) from its own slots
-  return run_dequant(d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 0));
+  return run_dequant(d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 0), nullptr, lat);
+}
+
+qsdp_status qsdp_reduce_scatter_lattice(qsdp_comm* c, const void* full_grad, int32_t in_dtype, const qsdp_segment* segs,
+                                        const qsdp_key* key, void* shard_out, int32_t out_dtype, void* x_shard,
+                                        const qsdp_lattice* lat, void* stream) {
+  qsdp_status st = check_lattice(lat, x_shard);
+  if (st != QSDP_OK) return st;
+  return reduce_scatter_impl(c, full_grad, in_dtype, segs, key, shard_out, out_dtype, stream, x_shard, lat);
 }
 
 }  // extern "C"

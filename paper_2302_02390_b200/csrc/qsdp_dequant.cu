@@ -7,6 +7,13 @@ static cudaError_t launch_d_tl(const DJobTable& tab, bool vec, int sms, cudaStre
   auto go = [&](auto kern) {
     kern<<<persistent_grid(kern, 256, 0, tab.total_buckets, 32 / TL, sms), 256, 0, s>>>(tab);
   };
+  if constexpr (ACC) {
+    if (tab.lat_on) {  // K4 with the fused lattice-projected step
+      if (vec) go(dequant_kernel<BITS, TL, OUT, true, ACC, true>);
+      else go(dequant_kernel<BITS, TL, OUT, false, ACC, true>);
+      return cudaGetLastError();
+    }
+  }
   if (vec) go(dequant_kernel<BITS, TL, OUT, true, ACC>);
   else go(dequant_kernel<BITS, TL, OUT, false, ACC>);
   return cudaGetLastError();
@@ -14,15 +21,20 @@ static cudaError_t launch_d_tl(const DJobTable& tab, bool vec, int sms, cudaStre
 
 template <int BITS, int OUT, bool ACC>
 static cudaError_t launch_d_bits(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
-  int tl = team_lanes(tab.bucket);
-  if (ACC && tl < 8) tl = 8;  // per-source scale rows are filled by lanes 0..nsrc-1
-  switch (tl) {
-    case 1: return launch_d_tl<BITS, 1, OUT, ACC>(tab, vec, sms, s);
-    case 2: return launch_d_tl<BITS, 2, OUT, ACC>(tab, vec, sms, s);
-    case 4: return launch_d_tl<BITS, 4, OUT, ACC>(tab, vec, sms, s);
-    case 8: return launch_d_tl<BITS, 8, OUT, ACC>(tab, vec, sms, s);
-    case 16: return launch_d_tl<BITS, 16, OUT, ACC>(tab, vec, sms, s);
-    default: return launch_d_tl<BITS, 32, OUT, ACC>(tab, vec, sms, s);
+  const int tl = team_lanes(tab.bucket);
+  if constexpr (ACC) {  // per-source scale rows are filled by lanes 0..nsrc-1: teams of >= 8 lanes
+    if (tl <= 8) return launch_d_tl<BITS, 8, OUT, ACC>(tab, vec, sms, s);
+    if (tl == 16) return launch_d_tl<BITS, 16, OUT, ACC>(tab, vec, sms, s);
+    return launch_d_tl<BITS, 32, OUT, ACC>(tab, vec, sms, s);
+  } else {
+    switch (tl) {
+      case 1: return launch_d_tl<BITS, 1, OUT, ACC>(tab, vec, sms, s);
+      case 2: return launch_d_tl<BITS, 2, OUT, ACC>(tab, vec, sms, s);
+      case 4: return launch_d_tl<BITS, 4, OUT, ACC>(tab, vec, sms, s);
+      case 8: return launch_d_tl<BITS, 8, OUT, ACC>(tab, vec, sms, s);
+      case 16: return launch_d_tl<BITS, 16, OUT, ACC>(tab, vec, sms, s);
+      default: return launch_d_tl<BITS, 32, OUT, ACC>(tab, vec, sms, s);
+    }
   }
 }
 

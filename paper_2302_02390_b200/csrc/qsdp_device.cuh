@@ -223,7 +223,8 @@ struct QJobTable {
 struct DJob {
   const uint8_t* codes[8];  // sources (1 for plain dequant; P for dequant-accumulate)
   const float* meta[8];
-  void* out;
+  void* out;                // may be nullptr for a lattice step (then only x moves)
+  void* lat_x;              // lattice step: this job's iterate (in / out)
   int64_t length;
   int64_t bucket_base;
   int32_t nsrc;
@@ -243,6 +244,14 @@ struct DJobTable {
   int32_t parity_adj;
   const unsigned long long* parity_ptr;  // sources move by ((*p + adj) & 1) * parity_stride bytes
   int64_t parity_stride;
+  // Lattice-projected step fused into K4 (optimizer.py:194-229): with the averaged
+  // gradient g, x <- d * rint((x - c*g - r) / d) + r, r = uniform(-d/2, d/2) drawn
+  // from the keyed stream lat_key (step += *lat_step_ptr when set), start 0.
+  int32_t lat_on;
+  int32_t lat_xdtype;  // 0 f32, 1 f64
+  double lat_c, lat_d;
+  uint64_t lat_key[5];
+  const unsigned long long* lat_step_ptr;
 };
 
 // Synchronisation words of a fused single-launch collective (see fused_collective_kernel).

@@ -1235,6 +1235,41 @@ __device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, c
   }
 }
 
+// The lattice shift of this call: r = sample_shift(d, bucket_rng(key..., 0))
+// = -d/2 + d * random() (quantize.py:130-132, numpy's unfused uniform).
+static __device__ __noinline__ double lattice_shift(const DJobTable& tab) {
+  const uint64_t step = tab.lat_key[1] + (tab.lat_step_ptr ? ld_dev_u64(tab.lat_step_ptr) : 0ull);
+  const SeedPrefix pre = make_prefix(tab.lat_key[0], step, tab.lat_key[2], tab.lat_key[3], tab.lat_key[4]);
+  U128 s0, inc;
+  seed_bucket(pre, 0, s0, inc);
+  const U128 s1 = mad128(s0, pcg_mult(), inc);
+  const double u = u64_to_unit_double(pcg_output(s1));
+  return __dadd_rn(__dmul_rn(tab.lat_d, -0.5), __dmul_rn(tab.lat_d, u));
+}
+
+// K4 epilogue: the averaged gradient g goes to J.out (when set) and, for a
+// lattice step, the owner's iterate moves to d * rint((x - c*g - r)/d) + r
+// (qsdp_step, optimizer.py:212-216; np.round = half to even), in fp64.
+template <int OUT, bool VEC, bool LAT>
+__device__ __forceinline__ void acc_store4(const DJobTable& tab, const DJob& J, int64_t idx, int n_left,
+                                           const double g[4], double lat_r) {
+  if (!LAT || J.out != nullptr) store_out4<OUT, VEC>(J.out, idx, n_left, g);
+  if constexpr (LAT) {
+    const double c = tab.lat_c, d = tab.lat_d;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i >= n_left) break;
+      double x = tab.lat_xdtype == 1 ? reinterpret_cast<const double*>(J.lat_x)[idx + i]
+                                     : (double)reinterpret_cast<const float*>(J.lat_x)[idx + i];
+      const double y = __dsub_rn(x, __dmul_rn(c, g[i]));
+      const double q = rint(__ddiv_rn(__dsub_rn(y, lat_r), d));
+      x = __dadd_rn(__dmul_rn(d, q), lat_r);
+      if (tab.lat_xdtype == 1) reinterpret_cast<double*>(J.lat_x)[idx + i] = x;
+      else reinterpret_cast<float*>(J.lat_x)[idx + i] = __double2float_rn(x);
+    }
+  }
+}
+
 // K3: one source per job.  K4 (ACC): nsrc sources summed in order in fp64
 // starting from +0.0, then divided by `divisor` (acc = zeros; acc = acc + vals;
 // acc / P -- sharded.py:385-431).  Per-source scales of the current bucket are
@@ -1243,8 +1278,9 @@ __device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, c
 // One warp per bucket, S % 128 == 0 (every lane owns S/128 full groups of 4).
 // ADD0: K4 with a single source and divisor 1 -- out = (0.0 + val) / 1 (the
 // reference's zeros + vals; only the sign of a zero can differ from val).
-template <int BITS, int OUT, bool COH, bool ADD0 = false>
-__device__ __forceinline__ void dequant_fast32(const DJobTable& tab, int64_t poff, int64_t warp, int64_t nwarps) {
+template <int BITS, int OUT, bool COH, bool ADD0 = false, bool LAT = false>
+__device__ __forceinline__ void dequant_fast32(const DJobTable& tab, int64_t poff, int64_t warp, int64_t nwarps,
+                                               double lat_r = 0.0) {
   constexpr int UMAX = 8;
   const int lane = threadIdx.x & 31;
   const int S = tab.bucket;
@@ -1298,7 +1334,8 @@ __device__ __forceinline__ void dequant_fast32(const DJobTable& tab, int64_t pof
           v[i] = __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift);  // (lo + code*pitch) + shift
           if (ADD0) v[i] = __dadd_rn(0.0, v[i]);
         }
-        store_out4<OUT, true>(J.out, off + e, cur.n - e, v);
+        if (ADD0) acc_store4<OUT, true, LAT>(tab, J, off + e, cur.n - e, v, lat_r);
+        else store_out4<OUT, true>(J.out, off + e, cur.n - e, v);
       }
     }
     b = bn;
@@ -1314,9 +1351,9 @@ __device__ __forceinline__ void dequant_fast32(const DJobTable& tab, int64_t pof
 // Per-source scales live in shared memory rows (lanes < nsrc fill them).
 // A power-of-two divisor is applied as a multiply by its exact reciprocal
 // (bit-identical to the division); other divisors divide.
-template <int BITS, int OUT, bool COH, int NSMAX>
+template <int BITS, int OUT, bool COH, int NSMAX, bool LAT>
 __device__ __forceinline__ void dequant_acc_fast32(const DJobTable& tab, int64_t poff, int64_t warp, int64_t nwarps,
-                                                   double (*row)[3]) {
+                                                   double (*row)[3], double lat_r) {
   constexpr int UC = 16 / NSMAX;
   const int lane = threadIdx.x & 31;
   const int S = tab.bucket;
@@ -1379,15 +1416,15 @@ __device__ __forceinline__ void dequant_acc_fast32(const DJobTable& tab, int64_t
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             acc[u][i] = pow2 ? __dmul_rn(acc[u][i], rdiv) : __ddiv_rn(acc[u][i], (double)dv);
-          store_out4<OUT, true>(J.out, off + e, n - e, acc[u]);
+          acc_store4<OUT, true, LAT>(tab, J, off + e, n - e, acc[u], lat_r);
         }
       }
     }
   }
 }
 
-template <int BITS, int TL, int OUT, bool VEC, bool ACC, bool COH = false>
-__device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_meta_base) {
+template <int BITS, int TL, int OUT, bool VEC, bool ACC, bool COH = false, bool LAT = false>
+__device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_meta_base, double lat_r = 0.0) {
   const int64_t poff = d_parity_off(tab);
   constexpr int TEAMS = 32 / TL;
   constexpr int U = 8;  // groups whose code words are loaded before use
@@ -1415,7 +1452,7 @@ __device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_me
       for (int j = 0; j < tab.njobs && single; ++j) single = tab.jobs[j].nsrc == 1;
     }
     if (single && cvec && (S & 127) == 0 && S <= 1024) {
-      dequant_fast32<BITS, OUT, COH, ACC>(tab, poff, warp, nwarps);
+      dequant_fast32<BITS, OUT, COH, ACC, LAT>(tab, poff, warp, nwarps, lat_r);
       return;
     }
     if constexpr (ACC) {
@@ -1423,9 +1460,9 @@ __device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_me
       for (int j = 0; j < tab.njobs; ++j) ns = max(ns, tab.jobs[j].nsrc);
       if (cvec && (S & 127) == 0 && S <= 1024 && ns <= 8) {
         double(*row)[3] = reinterpret_cast<double(*)[3]>(sm_meta_base + ((size_t)wib * TEAMS * 8) * 3);
-        if (ns <= 2) dequant_acc_fast32<BITS, OUT, COH, 2>(tab, poff, warp, nwarps, row);
-        else if (ns <= 4) dequant_acc_fast32<BITS, OUT, COH, 4>(tab, poff, warp, nwarps, row);
-        else dequant_acc_fast32<BITS, OUT, COH, 8>(tab, poff, warp, nwarps, row);
+        if (ns <= 2) dequant_acc_fast32<BITS, OUT, COH, 2, LAT>(tab, poff, warp, nwarps, row, lat_r);
+        else if (ns <= 4) dequant_acc_fast32<BITS, OUT, COH, 4, LAT>(tab, poff, warp, nwarps, row, lat_r);
+        else dequant_acc_fast32<BITS, OUT, COH, 8, LAT>(tab, poff, warp, nwarps, row, lat_r);
         return;
       }
     }
@@ -1535,7 +1572,7 @@ __device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_me
 #pragma unroll
               for (int i = 0; i < 4; ++i) acc[u][i] = __ddiv_rn(acc[u][i], (double)tab.divisor);
             }
-            store_out4<OUT, VEC>(J.out, off + e, n - e, acc[u]);
+            acc_store4<OUT, VEC, LAT>(tab, J, off + e, n - e, acc[u], lat_r);
           }
         }
       }
@@ -1544,10 +1581,16 @@ __device__ __forceinline__ void dequant_body(const DJobTable& tab, double* sm_me
   }
 }
 
-template <int BITS, int TL, int OUT, bool VEC, bool ACC>
+template <int BITS, int TL, int OUT, bool VEC, bool ACC, bool LAT = false>
 __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJobTable tab) {
   __shared__ double sm_meta[ACC ? 8 * (32 / TL) * 8 * 3 : 1];
-  dequant_body<BITS, TL, OUT, VEC, ACC, false>(tab, sm_meta);
+  double lat_r = 0.0;
+  if constexpr (LAT) {  // one keyed draw per warp (lane 0), broadcast by shuffle
+    double r = 0.0;
+    if ((threadIdx.x & 31) == 0) r = lattice_shift(tab);
+    lat_r = __shfl_sync(0xffffffffu, r, 0);
+  }
+  dequant_body<BITS, TL, OUT, VEC, ACC, false, LAT>(tab, sm_meta, lat_r);
 }
 
 // ---------------------------------------------------------------------------

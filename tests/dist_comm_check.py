@@ -98,6 +98,7 @@ def main():
                 print(f"rank {rank} size {size} graph replay {rep}: mismatch", flush=True)
         comm.close()
     failures += levels_all_gather(rank, world, dev)
+    failures += lattice_reduce_scatter(rank, world, dev)
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
     if rank == 0:
@@ -130,6 +131,33 @@ def levels_all_gather(rank, world, dev):
                 fails += 1
                 print(f"rank {rank} levels size {size} step {step}: mismatch", flush=True)
         comm.close()
+    return fails
+
+
+def lattice_reduce_scatter(rank, world, dev):
+    """C2 + the fused lattice step on every owner's shard (SURVEY §8(f) #4) vs the oracle."""
+    from paper_2302_02390_b200.lattice import LatticeStep, shift_key
+    fails = 0
+    size, bucket, gb, d, cc = 700001, 1024, 8, 2e-4, 0.3
+    segs = plan_segments(size, world, bucket)
+    comm = QSDPComm(max(n for _, n in segs), QuantSpec(8, bucket, "shift"), QuantSpec(gb, bucket, "uniform_stochastic"))
+    grads = [(np.random.default_rng(50 + p).standard_normal(size) * 1e-3).astype(np.float32) for p in range(world)]
+    x_full = np.random.default_rng(99).standard_normal(size)
+    s, n = segs[rank]
+    x = torch.from_numpy(x_full[s:s + n].copy()).to(dev)
+    for step in range(2):
+        comm.reduce_scatter_lattice(torch.from_numpy(grads[rank]).to(dev), segs, SegmentKey(0, step, 6, 2, rank), x,
+                                    LatticeStep(cc, d, shift_key(0, step, 6)))
+        acc = np.zeros(n)
+        for p in range(world):
+            c, m, _ = O.quantize_segment(grads[p][s:s + n], s, bucket, gb, 1, (0, step, 6, 2, p), 8)
+            acc = acc + O.dequantize_segment(c, m, n, bucket, gb, 8)
+        r = -d / 2 + d * O.PCG64(0, step, 6, 3, 0, 0).random()
+        x_full[s:s + n] = d * np.round((x_full[s:s + n] - cc * (acc / world) - r) / d) + r
+        if not np.array_equal(x.cpu().numpy(), x_full[s:s + n]):
+            fails += 1
+            print(f"rank {rank} lattice step {step}: mismatch", flush=True)
+    comm.close()
     return fails
 
 

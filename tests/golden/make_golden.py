@@ -17,6 +17,11 @@ reference functions:
             including the re-sort / collision-nudge and distinct-count paths;
 * wire_*:   malformed / edge-case messages and the exception class (or "ok") the
             reference decode() raises for each (wire.py:134-184);
+* lat_*:    the lattice-projected step fused with the RS epilogue
+            (optimizer.py:194-229): the reduce-scatter average of P ranks'
+            quantized gradients (sharded.py:375-433 pipeline), then the
+            reference's qsdp_step with that gradient and the keyed shift
+            r = sample_shift(d, bucket_rng(root, step, layer, 3, 0, 0));
 * ledger_csv: CommLedger.to_csv bytes of a ShardedMLP run (sharded.py:161-181);
 * hook_*:   inputs/outputs of ShardedMLP._gather / ._reduce_scatter recorded
             during a short ShardedMLP run (sharded.py:323-433), plus the run's
@@ -161,6 +166,49 @@ def _levels(out):
     out["ll_lr"] = np.array(lrows)
 
 
+def _lattice_cases(out):
+    from qsdp.optimizer import RunPlan, qsdp_step
+    from qsdp.quantize import sample_shift
+    rng = np.random.default_rng(733)
+
+    class _Stub:  # a "problem" whose stochastic gradient is the reduce-scatter average
+        def __init__(self, g, beta):
+            self.g, self.smoothness = g, beta
+
+        def stochastic_gradient(self, x, rng):
+            return self.g
+
+        def objective(self, x):
+            return 0.0
+
+    rows = []
+    for k, (P, bits, S, n, eta, beta, dstar, ratio) in enumerate(
+            [(2, 8, 1024, 5000, 0.5, 2.0, 0.01, 64), (4, 4, 256, 3001, 0.3, 1.0, 0.001, 16),
+             (3, 8, 100, 777, 1.0, 4.0, 1e-4, 3), (1, 6, 64, 640, 0.25, 1.5, 0.05, 128)]):
+        root, step, layer = 5, 7 + k, 2
+        grads = [(rng.standard_normal(n) * 1e-2).astype(np.float32).astype(np.float64) for _ in range(P)]
+        acc = np.zeros(n)
+        for p in range(P):
+            blocks = _segment_blocks(grads[p], 0, S, bits, "uniform_stochastic",
+                                     lambda st, p=p: bucket_rng(root, step, layer, PHASE_GRAD, p, st))
+            acc = acc + np.concatenate([dequantize(b, "uniform_stochastic") for b in blocks])
+        ghat = acc / P
+        d = dstar / ratio
+        plan = RunPlan(eta=eta, coarse_resolution=dstar, fine_resolution=d, iteration_count=1, epsilon=1.0,
+                       grid_ratio=ratio)
+        r = sample_shift(d, bucket_rng(root, step, layer, 3, 0, 0))
+        x = rng.standard_normal(n) * 0.1
+        x_new, rec = qsdp_step(x, _Stub(ghat, beta), plan, rng, shift=r)
+        assert rec.shift == r
+        out[f"lat_{k}_grads"] = np.stack(grads).astype(np.float32)
+        out[f"lat_{k}_x"] = x
+        out[f"lat_{k}_ghat"] = ghat
+        out[f"lat_{k}_xnew"] = x_new
+        out[f"lat_{k}_r"] = np.array(r)
+        rows.append([P, bits, S, n, root, step, layer, eta, beta, d])
+    out["lat_cases"] = np.array(rows, dtype=np.float64)
+
+
 def _wire_cases(out):
     from qsdp.quantize import QuantizedBlock
     from qsdp.wire import decode
@@ -302,6 +350,7 @@ def main():
     out["n_hooks"] = np.array(hook_idx)
     _levels(out)
     _wire_cases(out)
+    _lattice_cases(out)
     out["n_runs"] = np.array(len(hook_rows))
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {os.path.getsize(OUT)/1e6:.2f} MB, {len(cases)} quant cases, "

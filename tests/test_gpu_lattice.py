@@ -1,0 +1,82 @@
+"""Lattice-projected step fused with the RS epilogue vs the
+reference's qsdp_step (optimizer.py:194-229) on golden vectors, and the
+collective form vs the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _lat_cases(g):
+    for k, row in enumerate(g["lat_cases"]):
+        P, bits, S, n, root, step, layer = (int(v) for v in row[:7])
+        eta, beta, d = (float(v) for v in row[7:])
+        yield dict(k=k, P=P, bits=bits, S=S, n=n, root=root, step=step, layer=layer, eta=eta, beta=beta, d=d,
+                   grads=g[f"lat_{k}_grads"], x=g[f"lat_{k}_x"], ghat=g[f"lat_{k}_ghat"], xnew=g[f"lat_{k}_xnew"],
+                   r=float(g[f"lat_{k}_r"]))
+
+
+def _sources(c):
+    from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey, quantize_segments
+    spec = QuantSpec(c["bits"], c["S"], "uniform_stochastic")
+    items = [(torch.from_numpy(c["grads"][p].copy()).cuda(), 0, SegmentKey(c["root"], c["step"], c["layer"], 2, p))
+             for p in range(c["P"])]
+    return spec, quantize_segments(items, spec)
+
+
+def test_lattice_step_golden_f64(golden):
+    from paper_2302_02390_b200.lattice import LatticeStep, dequant_accumulate_lattice, shift_key
+    for c in _lat_cases(golden):
+        spec, src = _sources(c)
+        x = torch.from_numpy(c["x"].copy()).cuda()
+        g = torch.empty(c["n"], dtype=torch.float64, device="cuda")
+        step = LatticeStep(c["eta"] / c["beta"], c["d"], shift_key(c["root"], c["step"], c["layer"]))
+        dequant_accumulate_lattice(src, c["n"], spec, c["P"], x, step, g_out=g)
+        np.testing.assert_array_equal(g.cpu().numpy(), c["ghat"], err_msg=f"lattice case {c['k']}: gradient")
+        np.testing.assert_array_equal(x.cpu().numpy(), c["xnew"], err_msg=f"lattice case {c['k']}: iterate")
+
+
+def test_lattice_step_f32_iterate(golden):
+    """fp32 parameters: the fp64 step of float64(x), rounded to float32."""
+    from paper_2302_02390_b200.lattice import LatticeStep, dequant_accumulate_lattice, shift_key
+    for c in _lat_cases(golden):
+        spec, src = _sources(c)
+        x32 = c["x"].astype(np.float32)
+        x = torch.from_numpy(x32.copy()).cuda()
+        cc = c["eta"] / c["beta"]
+        dequant_accumulate_lattice(src, c["n"], spec, c["P"], x, LatticeStep(cc, c["d"],
+                                                                            shift_key(c["root"], c["step"], c["layer"])))
+        y = x32.astype(np.float64) - cc * c["ghat"]
+        exp = (c["d"] * np.round((y - c["r"]) / c["d"]) + c["r"]).astype(np.float32)
+        np.testing.assert_array_equal(x.cpu().numpy(), exp)
+
+
+def test_shift_matches_keyed_stream(oracle, golden):
+    for c in _lat_cases(golden):
+        u = oracle.PCG64(c["root"], c["step"], c["layer"], 3, 0, 0).random()
+        assert c["r"] == -c["d"] / 2 + c["d"] * u
+
+
+def test_comm_lattice_single_rank(oracle):
+    from paper_2302_02390_b200.comm import QSDPComm
+    from paper_2302_02390_b200.lattice import LatticeStep, shift_key
+    from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey
+    dev = torch.device("cuda", 0)
+    n, S = 1024 * 50 + 3, 1024
+    comm = QSDPComm(n, QuantSpec(8, S, "shift"), QuantSpec(8, S, "uniform_stochastic"), device=dev)
+    g = (np.random.default_rng(1).standard_normal(n) * 1e-3).astype(np.float32)
+    x0 = np.random.default_rng(2).standard_normal(n)
+    x = torch.from_numpy(x0.copy()).to(dev)
+    gout = torch.empty(n, dtype=torch.float64, device=dev)
+    d, cc = 1e-4, 0.25
+    comm.reduce_scatter_lattice(torch.from_numpy(g).to(dev), [(0, n)], SegmentKey(0, 4, 1, 2, 0), x,
+                                LatticeStep(cc, d, shift_key(0, 4, 1)), out=gout)
+    codes, meta, _ = oracle.quantize_segment(g, 0, S, 8, 1, (0, 4, 1, 2, 0), 8)
+    ghat = (np.zeros(n) + oracle.dequantize_segment(codes, meta, n, S, 8, 8)) / 1
+    r = -d / 2 + d * oracle.PCG64(0, 4, 1, 3, 0, 0).random()
+    exp = d * np.round((x0 - cc * ghat - r) / d) + r
+    np.testing.assert_array_equal(gout.cpu().numpy(), ghat)
+    np.testing.assert_array_equal(x.cpu().numpy(), exp)
+    comm.close()
