@@ -474,6 +474,31 @@ def main():
         wire["decode"] = {"ms_per_pass": round(tk, 4), "gbs": round(2 * mbytes / (tk * 1e-3) / 1e9, 1),
                           "bytes_per_pass": 2 * mbytes}
 
+    # ---- K4 with the fused lattice-projected step (world 1) ----
+    lattice = None
+    if world == 1 and not args.no_levels:
+        from paper_2302_02390_b200.lattice import LatticeStep, dequant_accumulate_lattice, shift_key
+        for gi, st in enumerate(state):
+            quantize_segments([(st["grad"], 0, SegmentKey(0, 0, gi, 2, 0))], gspec, out=[st["gq"]])
+            st["x"] = torch.randn(st["g"].numel, generator=gen, device=dev).mul_(0.02)
+        lsteps = [LatticeStep(0.25, 1e-4, shift_key(0, 0, gi)) for gi in range(len(state))]
+
+        def lat_all():
+            for st, ls in zip(state, lsteps):
+                dequant_accumulate_lattice([st["gq"]], st["g"].numel, gspec, 1, st["x"], ls)
+
+        lb = sum(codes_bytes(st["g"].numel, gspec) + 12 * num_buckets(st["g"].numel, args.bucket)
+                 + 8 * st["g"].numel for st in state)  # codes + meta in, fp32 iterate read + written
+        gk = capture(lat_all)
+        gk.replay()
+        torch.cuda.synchronize(dev)
+        evk = time_graph(gk, args.steps)
+        torch.cuda.synchronize(dev)
+        tk = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+        lattice = {"K4_lattice_step": {"ms_per_pass": round(tk, 4), "gbs": round(lb / (tk * 1e-3) / 1e9, 1),
+                                       "frac_of_hbm_peak": round(lb / (tk * 1e-3) / 1e9 / hbm_peak, 4),
+                                       "bytes_per_pass": lb, "x_dtype": "f32", "launches_per_pass": len(state)}}
+
     # ---- e2e: through the C-ABI communicator, host buffers, copies inside the timed region ----
     e2e = None
     if not args.no_e2e:
@@ -555,7 +580,7 @@ def main():
                                     + ("fused single-launch collectives" if comm_fused else "3 launches per collective"),
                        "convention": "sum over ranks of 4*N per collective / time"},
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
-            "levels": levels, "wire": wire,
+            "levels": levels, "wire": wire, "lattice": lattice,
             "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

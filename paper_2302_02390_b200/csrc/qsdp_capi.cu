@@ -250,6 +250,7 @@ void build_dtab(DJobTable& tab, const std::vector<DJobSpec>& jobs, size_t& i, co
     tab.lat_xdtype = lat->x_dtype == QSDP_F64 ? 1 : 0;
     tab.lat_c = lat->lr_over_beta;
     tab.lat_d = lat->delta;
+    tab.lat_inv_d = 1.0 / lat->delta;
     tab.lat_key[0] = lat->shift_key.root_seed;
     tab.lat_key[1] = lat->shift_key.step;
     tab.lat_key[2] = lat->shift_key.layer;

@@ -9,6 +9,21 @@ static cudaError_t launch_d_tl(const DJobTable& tab, bool vec, int sms, cudaStre
   };
   if constexpr (ACC) {
     if (tab.lat_on) {  // K4 with the fused lattice-projected step
+      if constexpr (TL == 32 && (BITS == 8 || BITS == 4)) {
+        int ns = 0;
+        for (int j = 0; j < tab.njobs; ++j) ns = ns > tab.jobs[j].nsrc ? ns : tab.jobs[j].nsrc;
+        if (vec && tab.codes_vec && (tab.bucket & 127) == 0 && tab.bucket <= 1024) {
+          auto pick = [&](auto xt) {
+            using XT = decltype(xt);
+            if (ns <= 2) go(dequant_lat_fast_kernel<BITS, OUT, 2, XT>);
+            else if (ns <= 4) go(dequant_lat_fast_kernel<BITS, OUT, 4, XT>);
+            else go(dequant_lat_fast_kernel<BITS, OUT, 8, XT>);
+          };
+          if (tab.lat_xdtype == 1) pick(0.0);
+          else pick(0.0f);
+          return cudaGetLastError();
+        }
+      }
       if (vec) go(dequant_kernel<BITS, TL, OUT, true, ACC, true>);
       else go(dequant_kernel<BITS, TL, OUT, false, ACC, true>);
       return cudaGetLastError();

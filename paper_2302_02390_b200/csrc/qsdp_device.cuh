@@ -249,7 +249,7 @@ struct DJobTable {
   // from the keyed stream lat_key (step += *lat_step_ptr when set), start 0.
   int32_t lat_on;
   int32_t lat_xdtype;  // 0 f32, 1 f64
-  double lat_c, lat_d;
+  double lat_c, lat_d, lat_inv_d;  // lat_inv_d = fl(1/d) (certified rounding, exact fallback)
   uint64_t lat_key[5];
   const unsigned long long* lat_step_ptr;
 };

@@ -1255,18 +1255,100 @@ __device__ __forceinline__ void acc_store4(const DJobTable& tab, const DJob& J, 
                                            const double g[4], double lat_r) {
   if (!LAT || J.out != nullptr) store_out4<OUT, VEC>(J.out, idx, n_left, g);
   if constexpr (LAT) {
-    const double c = tab.lat_c, d = tab.lat_d;
+    const double c = tab.lat_c, d = tab.lat_d, inv_d = tab.lat_inv_d;
+    const bool vx = VEC && n_left >= 4 && (((uintptr_t)J.lat_x & 15) == 0);
+    double x[4];
+    if (tab.lat_xdtype == 1) {
+      const double* xp = reinterpret_cast<const double*>(J.lat_x) + idx;
+      if (vx) {
+        const double2 a = reinterpret_cast<const double2*>(xp)[0], b = reinterpret_cast<const double2*>(xp)[1];
+        x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+      } else {
+        for (int i = 0; i < 4; ++i) x[i] = i < n_left ? xp[i] : 0.0;
+      }
+    } else {
+      const float* xp = reinterpret_cast<const float*>(J.lat_x) + idx;
+      if (vx) {
+        const float4 a = *reinterpret_cast<const float4*>(xp);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+      } else {
+        for (int i = 0; i < 4; ++i) x[i] = i < n_left ? (double)xp[i] : 0.0;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      if (i >= n_left) break;
-      double x = tab.lat_xdtype == 1 ? reinterpret_cast<const double*>(J.lat_x)[idx + i]
-                                     : (double)reinterpret_cast<const float*>(J.lat_x)[idx + i];
-      const double y = __dsub_rn(x, __dmul_rn(c, g[i]));
-      const double q = rint(__ddiv_rn(__dsub_rn(y, lat_r), d));
-      x = __dadd_rn(__dmul_rn(d, q), lat_r);
-      if (tab.lat_xdtype == 1) reinterpret_cast<double*>(J.lat_x)[idx + i] = x;
-      else reinterpret_cast<float*>(J.lat_x)[idx + i] = __double2float_rn(x);
+      // z = (y - r) / d in fp64; rint(z) from z' = (y - r) * fl(1/d) (|z' - z| < 3.5e-16 |z|)
+      // unless z' is within 4e-16 |z'| of a half-integer or too large for the test
+      const double a = __dsub_rn(__dsub_rn(x[i], __dmul_rn(c, g[i])), lat_r);
+      const double z1 = __dmul_rn(a, inv_d);
+      const double fz = floor(z1), t = __dsub_rn(z1, fz);
+      double q = t < 0.5 ? fz : __dadd_rn(fz, 1.0);
+      if (fabs(__dsub_rn(t, 0.5)) <= 4e-16 * fabs(z1) || !(fabs(z1) < 0x1p51)) q = rint(__ddiv_rn(a, d));
+      x[i] = __dadd_rn(__dmul_rn(d, q), lat_r);
     }
+    if (tab.lat_xdtype == 1) {
+      double* xp = reinterpret_cast<double*>(J.lat_x) + idx;
+      if (vx) {
+        reinterpret_cast<double2*>(xp)[0] = make_double2(x[0], x[1]);
+        reinterpret_cast<double2*>(xp)[1] = make_double2(x[2], x[3]);
+      } else {
+        for (int i = 0; i < 4 && i < n_left; ++i) xp[i] = x[i];
+      }
+    } else {
+      float* xp = reinterpret_cast<float*>(J.lat_x) + idx;
+      if (vx) {
+        *reinterpret_cast<float4*>(xp) = make_float4(__double2float_rn(x[0]), __double2float_rn(x[1]),
+                                                     __double2float_rn(x[2]), __double2float_rn(x[3]));
+      } else {
+        for (int i = 0; i < 4 && i < n_left; ++i) xp[i] = __double2float_rn(x[i]);
+      }
+    }
+  }
+}
+
+// Lattice move of 4 iterate values already in registers (see acc_store4).
+__device__ __forceinline__ void lat_move4(const DJobTable& tab, double x[4], const double g[4], double lat_r) {
+  const double c = tab.lat_c, d = tab.lat_d, inv_d = tab.lat_inv_d;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double a = __dsub_rn(__dsub_rn(x[i], __dmul_rn(c, g[i])), lat_r);
+    const double z1 = __dmul_rn(a, inv_d);
+    const double fz = floor(z1), t = __dsub_rn(z1, fz);
+    double q = t < 0.5 ? fz : __dadd_rn(fz, 1.0);
+    if (fabs(__dsub_rn(t, 0.5)) <= 4e-16 * fabs(z1) || !(fabs(z1) < 0x1p51)) q = rint(__ddiv_rn(a, d));
+    x[i] = __dadd_rn(__dmul_rn(d, q), lat_r);
+  }
+}
+
+template <typename XT>
+__device__ __forceinline__ void lat_load4(const void* base, int64_t idx, int n_left, XT x[4]) {
+  const XT* p = reinterpret_cast<const XT*>(base) + idx;
+  if (n_left >= 4 && (((uintptr_t)p & 15) == 0)) {
+    if constexpr (sizeof(XT) == 4) {
+      const float4 a = *reinterpret_cast<const float4*>(p);
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    } else {
+      const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+      x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+    }
+  } else {
+    for (int i = 0; i < 4; ++i) x[i] = i < n_left ? p[i] : XT(0);
+  }
+}
+
+template <typename XT>
+__device__ __forceinline__ void lat_store4(void* base, int64_t idx, int n_left, const double x[4]) {
+  XT* p = reinterpret_cast<XT*>(base) + idx;
+  if (n_left >= 4 && (((uintptr_t)p & 15) == 0)) {
+    if constexpr (sizeof(XT) == 4) {
+      *reinterpret_cast<float4*>(p) = make_float4(__double2float_rn(x[0]), __double2float_rn(x[1]),
+                                                  __double2float_rn(x[2]), __double2float_rn(x[3]));
+    } else {
+      reinterpret_cast<double2*>(p)[0] = make_double2(x[0], x[1]);
+      reinterpret_cast<double2*>(p)[1] = make_double2(x[2], x[3]);
+    }
+  } else {
+    for (int i = 0; i < 4 && i < n_left; ++i) p[i] = (XT)x[i];
   }
 }
 
@@ -1417,6 +1499,88 @@ __device__ __forceinline__ void dequant_acc_fast32(const DJobTable& tab, int64_t
           for (int i = 0; i < 4; ++i)
             acc[u][i] = pow2 ? __dmul_rn(acc[u][i], rdiv) : __ddiv_rn(acc[u][i], (double)dv);
           acc_store4<OUT, true, LAT>(tab, J, off + e, n - e, acc[u], lat_r);
+        }
+      }
+    }
+  }
+}
+
+// K4 + lattice step (fast configuration): as dequant_acc_fast32, with the
+// iterate's values of a chunk loaded together with its code words, so one
+// memory round trip per chunk serves both (XT = iterate dtype).
+template <int BITS, int OUT, int NSMAX, typename XT>
+__device__ __forceinline__ void dequant_lat_fast32(const DJobTable& tab, int64_t poff, int64_t warp, int64_t nwarps,
+                                                   double (*row)[3], double lat_r) {
+  constexpr int UC = 16 / NSMAX < 4 ? 16 / NSMAX : 4;  // groups per chunk (wider measured slower: registers)
+  const int lane = threadIdx.x & 31;
+  const int S = tab.bucket;
+  const int G = S >> 7;
+  const double top = (double)((1u << BITS) - 1u);
+  const int64_t pbs = payload_bytes(S, BITS);
+  const int dv = tab.divisor;
+  const bool pow2 = (dv & (dv - 1)) == 0;
+  const double rdiv = 1.0 / (double)dv;
+  for (int64_t b = warp; b < tab.total_buckets; b += nwarps) {
+    const int j = find_job_d(tab, b);
+    const DJob& J = tab.jobs[j];
+    const int nsrc = J.nsrc;
+    const int64_t lb = b - J.bucket_base, off = lb * S;
+    const int n = (int)min((int64_t)S, J.length - off);
+    __syncwarp();
+    if (lane < nsrc) {
+      const float* m = meta_at(J.meta[lane], poff) + 3 * lb;
+      const double lo = (double)m[1];
+      row[lane][0] = lo;
+      row[lane][1] = __ddiv_rn(__dsub_rn((double)m[2], lo), top);
+      row[lane][2] = (double)m[0];
+    }
+    __syncwarp();
+    for (int g0 = 0; g0 < G; g0 += UC) {
+      uint32_t w[NSMAX][UC];
+      XT xv[UC][4];  // the iterate in its own type until used
+#pragma unroll
+      for (int p = 0; p < NSMAX; ++p) {
+        const uint8_t* __restrict__ cp = J.codes[p < nsrc ? p : 0] + poff + lb * pbs;
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+          const int gi = (g0 + u) * 32 + lane;
+          w[p][u] = (p < nsrc && g0 + u < G && 4 * gi < n) ? (uint32_t)load_group_direct<BITS, false>(cp, gi) : 0u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int e = 4 * ((g0 + u) * 32 + lane);
+        if (g0 + u < G && e < n) lat_load4<XT>(J.lat_x, off + e, n - e, xv[u]);
+      }
+      double acc[UC][4];
+#pragma unroll
+      for (int u = 0; u < UC; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[u][i] = 0.0;
+#pragma unroll
+      for (int p = 0; p < NSMAX; ++p) {
+        if (p < nsrc) {
+          const double lo = row[p][0], pitch = row[p][1], shift = row[p][2];
+#pragma unroll
+          for (int u = 0; u < UC; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const double c = code_to_double((w[p][u] >> (i * BITS)) & ((1u << BITS) - 1u));
+              acc[u][i] = __dadd_rn(acc[u][i], __dadd_rn(__dadd_rn(lo, __dmul_rn(c, pitch)), shift));
+            }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int e = 4 * ((g0 + u) * 32 + lane);
+        if (g0 + u < G && e < n) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            acc[u][i] = pow2 ? __dmul_rn(acc[u][i], rdiv) : __ddiv_rn(acc[u][i], (double)dv);
+          if (J.out != nullptr) store_out4<OUT, true>(J.out, off + e, n - e, acc[u]);
+          double xd[4] = {(double)xv[u][0], (double)xv[u][1], (double)xv[u][2], (double)xv[u][3]};
+          lat_move4(tab, xd, acc[u], lat_r);
+          lat_store4<XT>(J.lat_x, off + e, n - e, xd);
         }
       }
     }
@@ -1591,6 +1755,21 @@ __global__ void __launch_bounds__(256) dequant_kernel(const __grid_constant__ DJ
     lat_r = __shfl_sync(0xffffffffu, r, 0);
   }
   dequant_body<BITS, TL, OUT, VEC, ACC, false, LAT>(tab, sm_meta, lat_r);
+}
+
+// K4 + lattice step, fast configuration only (TL 32, widths 8 / 4, S % 128 == 0,
+// S <= 1024, aligned buffers, nsrc <= NSMAX): its own kernel so its register
+// budget is that of this path alone (the general kernel's paths share one).
+template <int BITS, int OUT, int NSMAX, typename XT>
+__global__ void __launch_bounds__(256) dequant_lat_fast_kernel(const __grid_constant__ DJobTable tab) {
+  __shared__ double sm_meta[8 * 8 * 3];
+  double r = 0.0;
+  if ((threadIdx.x & 31) == 0) r = lattice_shift(tab);
+  const double lat_r = __shfl_sync(0xffffffffu, r, 0);
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double(*row)[3] = reinterpret_cast<double(*)[3]>(sm_meta + (size_t)(threadIdx.x >> 5) * 8 * 3);
+  dequant_lat_fast32<BITS, OUT, NSMAX, XT>(tab, d_parity_off(tab), warp, nwarps, row, lat_r);
 }
 
 // ---------------------------------------------------------------------------

@@ -80,3 +80,32 @@ def test_comm_lattice_single_rank(oracle):
     np.testing.assert_array_equal(gout.cpu().numpy(), ghat)
     np.testing.assert_array_equal(x.cpu().numpy(), exp)
     comm.close()
+
+
+def test_lattice_ties_and_near_ties():
+    """Iterates placed on / around half-integers of (y - r)/d exercise the exact
+    fallback of the certified rounding: results equal numpy's round (half-even)."""
+    from paper_2302_02390_b200.lattice import LatticeStep, dequant_accumulate_lattice, shift_key
+    from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey, quantize_segments
+    S, nb = 1024, 64
+    n = S * nb
+    spec = QuantSpec(8, S, "uniform_stochastic")
+    g0 = np.float32(0.0123)
+    src = quantize_segments([(torch.full((n,), float(g0), device="cuda"), 0, SegmentKey(1, 1, 1, 2, 0))], spec)
+    for d, cc in ((1e-3, 0.5), (0.1, 2.0), (3.0, 1.0), (2.0 ** -20, 0.125)):
+        step = LatticeStep(cc, d, shift_key(1, 1, 1))
+        r = float(torch.tensor(0.0))  # filled below from the device result of a zero move
+        base = np.arange(n, dtype=np.float64) - n / 2
+        # r is the keyed draw: recover it through the oracle-free identity x_new - d*q
+        import importlib
+        O = importlib.import_module("oracle.oracle")
+        r = -d / 2 + d * O.PCG64(1, 1, 1, 3, 0, 0).random()
+        y_half = (base + 0.5) * d + r  # (y - r)/d ~ k + 1/2
+        jitter = np.array([0.0, 1, -1, 2, -2, 1e3, -1e3])[np.arange(n) % 7] * np.finfo(np.float64).eps
+        y = y_half * (1 + jitter)
+        x0 = y + cc * float(g0)
+        x = torch.from_numpy(x0.copy()).cuda()
+        dequant_accumulate_lattice(src, n, spec, 1, x, step)
+        yy = x0 - cc * float(g0)
+        exp = d * np.round((yy - r) / d) + r
+        np.testing.assert_array_equal(x.cpu().numpy(), exp, err_msg=f"d={d}")
