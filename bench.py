@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gpt", action="store_true")
     ap.add_argument("--no-levels", action="store_true", help="skip the learned-levels kernel timings")
+    ap.add_argument("--serial", action="store_true",
+                    help="one stream for every collective (default: FSDP2's schedule, RS on its own stream/comm)")
     ap.add_argument("--gpt-steps", type=int, default=8)
     ap.add_argument("--gpt-batch", type=int, default=8, help="sequences per GPU")
     ap.add_argument("--gpt-seq", type=int, default=1024)
@@ -243,6 +245,11 @@ def main():
     step_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
     comm = QSDPComm(max_seg, wspec, gspec, device=dev)
     comm.set_step_source(step_ctr)
+    # FSDP2's schedule (fsdp.QSDPContext): reduce-scatters on their own stream with their own
+    # communicator, RS(i) after AG(i)'s backward re-gather, overlapping AG(i-1)
+    rs_comm = comm if args.serial else QSDPComm(max_seg, wspec, gspec, device=dev)
+    rs_comm.set_step_source(step_ctr)
+    rs_stream = torch.cuda.Stream(device=dev)
     comm_fused = os.environ.get("QSDP_FUSED", "0") == "1" and args.bucket % 8 == 0 and 128 <= args.bucket <= 2048 \
         and args.wbits in (2, 4, 8, 16) and args.gbits in (2, 4, 8, 16)
     stream = torch.cuda.current_stream(dev)
@@ -278,18 +285,36 @@ def main():
         return L
 
     def comm_launches():
+        """The step's collectives: (kind, launches, fn, on_rs_stream)."""
         L = []
         per = 3 if world > 1 else 2  # quantize (+ barrier) + dequant
         for gi, st in enumerate(state):
             L.append(("AG", per, lambda st=st, gi=gi: comm.all_gather(
-                st["shard"], st["segs"], SegmentKey(0, 0, gi, 0, 0), st["full"])))
+                st["shard"], st["segs"], SegmentKey(0, 0, gi, 0, 0), st["full"]), False))
         for gi in range(len(state) - 1, -1, -1):
             st = state[gi]
             L.append(("AG", per, lambda st=st, gi=gi: comm.all_gather(
-                st["shard"], st["segs"], SegmentKey(0, 0, gi, 1, 0), st["full"])))
-            L.append(("RS", per, lambda st=st, gi=gi: comm.reduce_scatter(
-                st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"])))
+                st["shard"], st["segs"], SegmentKey(0, 0, gi, 1, 0), st["full"]), False))
+            L.append(("RS", per, lambda st=st, gi=gi: rs_comm.reduce_scatter(
+                st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"]), not args.serial))
         return L
+
+    def issue(launches):
+        """Issue a step's collectives on the current stream (+ the RS stream, joined at the end)."""
+        main = torch.cuda.current_stream(dev)
+        forked = False
+        for _, _, fn, on_rs in launches:
+            if on_rs:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                rs_stream.wait_event(ev)
+                with torch.cuda.stream(rs_stream):
+                    fn()
+                forked = True
+            else:
+                fn()
+        if forked:
+            main.wait_stream(rs_stream)
 
     # `value` times the product path (the communicator: one fused launch per collective when
     # possible); the per-kernel roofline graphs replay the same kernels through the batch API.
@@ -300,8 +325,7 @@ def main():
 
     def run_step(sel=None):
         if sel is None:
-            for _, _, fn in launches:
-                fn()
+            issue(launches)
             advance_counter(step_ctr)
         else:
             for kind, _, fn in klaunches:
@@ -514,8 +538,7 @@ def main():
             for st, h in zip(state, host):
                 st["shard"].copy_(h["shard"], non_blocking=True)
                 st["grad"].copy_(h["grad"], non_blocking=True)
-            for _, _, fn in claunch:
-                fn()
+            issue(claunch)
             for st, h in zip(state, host):
                 h["res"][: st["n"]].copy_(st["gshard"][: st["n"]], non_blocking=True)
             advance_counter(step_ctr)
@@ -585,6 +608,8 @@ def main():
         }
         print(json.dumps(line), flush=True)
     comm.close()
+    if rs_comm is not comm:
+        rs_comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
