@@ -107,3 +107,15 @@ def test_multi_gpu_comm():
                         os.path.join(ROOT, "tests", "dist_comm_check.py")],
                        capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_hierarchical_comm():
+    """Two-level (inter-node / intra-node) C1/C2, every node shape
+    dividing the world size, bit-exact vs the oracle (tests/dist_hier_check.py)."""
+    n = min(4, torch.cuda.device_count())
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29534",
+                        os.path.join(ROOT, "tests", "dist_hier_check.py")],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
