@@ -526,21 +526,57 @@ def main():
     # ---- e2e: through the C-ABI communicator, host buffers, copies inside the timed region ----
     e2e = None
     if not args.no_e2e:
+        # Pinned host inputs (each group's shard and gradient) and results.  Inside one
+        # step the copies overlap the collectives and each other: shards H2D in forward
+        # order and gradients in backward order on a copy stream; each collective waits
+        # only for its own input; each reduced shard goes D2H on a second copy stream
+        # as soon as its RS finishes (full-duplex PCIe; nothing crosses steps).
         host = []
         for st in state:
             host.append(dict(shard=st["shard"].cpu().pin_memory(), grad=st["grad"].cpu().pin_memory(),
-                             res=torch.empty(st["gshard"].numel(), dtype=torch.float32).pin_memory()))
+                             res=torch.empty(max(st["n"], 1), dtype=torch.float32).pin_memory()))
         bi = sum(h["shard"].numel() * 4 + h["grad"].numel() * 4 for h in host)
         bo = sum(st["n"] * 4 for st in state)
-        claunch = comm_launches()
+        h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
         def step_e2e():
-            for st, h in zip(state, host):
-                st["shard"].copy_(h["shard"], non_blocking=True)
-                st["grad"].copy_(h["grad"], non_blocking=True)
-            issue(claunch)
-            for st, h in zip(state, host):
-                h["res"][: st["n"]].copy_(st["gshard"][: st["n"]], non_blocking=True)
+            main = torch.cuda.current_stream(dev)
+            fork = torch.cuda.Event()
+            fork.record(main)
+            h2d.wait_event(fork)
+            d2h.wait_event(fork)
+            ev_shard, ev_grad = [], {}
+            with torch.cuda.stream(h2d):
+                for st, h in zip(state, host):
+                    st["shard"].copy_(h["shard"], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(h2d)
+                    ev_shard.append(e)
+                for gi in range(len(state) - 1, -1, -1):
+                    state[gi]["grad"].copy_(host[gi]["grad"], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(h2d)
+                    ev_grad[gi] = e
+            for gi, st in enumerate(state):
+                main.wait_event(ev_shard[gi])
+                comm.all_gather(st["shard"], st["segs"], SegmentKey(0, 0, gi, 0, 0), st["full"])
+            rs_s = main if args.serial else rs_stream
+            for gi in range(len(state) - 1, -1, -1):
+                st, h = state[gi], host[gi]
+                comm.all_gather(st["shard"], st["segs"], SegmentKey(0, 0, gi, 1, 0), st["full"])
+                e = torch.cuda.Event()
+                e.record(main)
+                rs_s.wait_event(e)
+                rs_s.wait_event(ev_grad[gi])
+                with torch.cuda.stream(rs_s):
+                    rs_comm.reduce_scatter(st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"])
+                    done = torch.cuda.Event()
+                    done.record(rs_s)
+                d2h.wait_event(done)
+                with torch.cuda.stream(d2h):
+                    h["res"][: st["n"]].copy_(st["gshard"][: st["n"]], non_blocking=True)
+            for sidestream in (rs_stream, h2d, d2h):
+                main.wait_stream(sidestream)
             advance_counter(step_ctr)
 
         step_e2e()
@@ -557,8 +593,9 @@ def main():
             ems = float(t.item())
         e2e = {"value": round(world * 12.0 * N_total / (ems / args.steps * 1e-3) / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "ms_per_step": round(ems / args.steps, 3),
-               "path": "QSDPComm -> qsdp_all_gather / qsdp_reduce_scatter (C ABI), pinned host buffers, "
-                       "one CUDA graph per step"}
+               "path": "QSDPComm -> qsdp_all_gather / qsdp_reduce_scatter (C ABI), pinned host buffers; "
+                       "per-group H2D / D2H copies on two copy streams overlapping the collectives inside "
+                       "the step; one CUDA graph per step"}
 
     # ---- GPT step/s: FSDP2 training step, unquantized (fp32 NCCL) vs QSDP comms ----
     gpt = None
