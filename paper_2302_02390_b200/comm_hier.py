@@ -90,9 +90,6 @@ class HierComm:
         meta = buf[coff: coff + 12 * max(nb, 1)].view(torch.float32).view(max(nb, 1), 3)
         return codes[:cb], meta[:nb]
 
-    def _global_of(self, node, local):
-        return node * self.node_size + local
-
     # -- C1 ---------------------------------------------------------------------------
     def all_gather(self, shard: torch.Tensor, segs, key: SegmentKey, out: torch.Tensor) -> torch.Tensor:
         """``out`` (full tensor, element 0 = segs[0] start) receives every rank's

@@ -318,32 +318,6 @@ __device__ __forceinline__ void load_octet(const T* p, T v[8]) {
   }
 }
 
-// Store the 8 codes of octet o (8*bits bits = `bits` bytes at byte o*bits).
-__device__ __forceinline__ void store_octet_any(uint8_t* base, int64_t o, const uint32_t c[8], int bits) {
-  uint8_t* p = base + o * bits;
-  if (bits <= 8) {
-    uint64_t w = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w |= (uint64_t)c[i] << (i * bits);
-    if (bits == 8) *reinterpret_cast<unsigned long long*>(p) = w;
-    else if (bits == 4) *reinterpret_cast<uint32_t*>(p) = (uint32_t)w;
-    else if (bits == 2) *reinterpret_cast<uint16_t*>(p) = (uint16_t)w;
-    else if (bits == 1) *p = (uint8_t)w;
-    else
-      for (int k = 0; k < bits; ++k) p[k] = (uint8_t)(w >> (8 * k));
-  } else {
-    unsigned __int128 w = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w |= (unsigned __int128)c[i] << (i * bits);
-    if (bits == 16) {
-      reinterpret_cast<unsigned long long*>(p)[0] = (unsigned long long)w;
-      reinterpret_cast<unsigned long long*>(p)[1] = (unsigned long long)(w >> 64);
-    } else {
-      for (int k = 0; k < bits; ++k) p[k] = (uint8_t)(w >> (8 * k));
-    }
-  }
-}
-
 // One warp per bucket; full buckets (n == S == 256*G) are held in registers
 // (G octets per lane, vector loads), short tail buckets take the octet loop
 // with scalar loads.
