@@ -247,6 +247,10 @@ def main():
     comm.set_step_source(step_ctr)
     # FSDP2's schedule (fsdp.QSDPContext): reduce-scatters on their own stream with their own
     # communicator, RS(i) after AG(i)'s backward re-gather, overlapping AG(i-1)
+    if os.environ.get("QSDP_FUSED", "0") == "1":
+        # a fused collective holds a grid-wide barrier: it needs every CTA resident, so it
+        # must never share the GPU with another collective stream
+        args.serial = True
     rs_comm = comm if args.serial else QSDPComm(max_seg, wspec, gspec, device=dev)
     rs_comm.set_step_source(step_ctr)
     rs_stream = torch.cuda.Stream(device=dev)

@@ -169,7 +169,9 @@ class QSDPComm:
         _lib.check(_lib.lib().qsdp_comm_set_step_source(self._h, counter.data_ptr() if counter is not None else None))
 
     def set_fused(self, enable: bool) -> None:
-        """Single-launch fused collectives (default on when the configuration allows)."""
+        """Single-launch fused collectives (opt-in; env QSDP_FUSED=1 sets the default).
+        A fused collective holds a grid-wide barrier and needs every CTA resident:
+        use it only when no other collective runs concurrently on this GPU (one stream)."""
         _lib.check(_lib.lib().qsdp_comm_set_fused(self._h, 1 if enable else 0))
 
     def close(self):
