@@ -236,3 +236,83 @@ class QSDPComm:
                 self._h, full_grad.data_ptr(), _DTYPE_CODE[full_grad.dtype], arr, ctypes.byref(k),
                 out.data_ptr(), _DTYPE_CODE[out.dtype], torch.cuda.current_stream(self.device).cuda_stream))
         return out
+
+
+def split_segments(segs, bucket: int, chunks: int):
+    """Cut every rank's segment into ``chunks`` bucket-aligned sub-segments
+    (sub-segment j of each rank covers its buckets [j*nb/chunks, (j+1)*nb/chunks)).
+    Keys stay those of the whole collective: a bucket is keyed by its global start,
+    so the codes and scales are unchanged (sharded.py:243-248)."""
+    out = []
+    for j in range(chunks):
+        sub = []
+        for s, n in segs:
+            nb = -(-n // bucket) if n else 0
+            b0, b1 = nb * j // chunks, nb * (j + 1) // chunks
+            lo, hi = min(n, b0 * bucket), min(n, b1 * bucket)
+            sub.append((s + lo, hi - lo))
+        out.append(sub)
+    return out
+
+
+class PipelinedComm:
+    """C1 / C2 of large tensors as ``chunks`` bucket-aligned sub-collectives that
+    alternate between two communicators on two streams, so one chunk's
+    quantize + NVLink push overlaps the previous chunk's dequantization (the two
+    phases of a single collective cannot overlap each other).  Results are
+    bit-identical to one QSDPComm call."""
+
+    def __init__(self, max_segment_elems: int, wspec: QuantSpec, gspec: QuantSpec, chunks: int = 4,
+                 group: dist.ProcessGroup | None = None, device: torch.device | None = None):
+        self.chunks = max(1, int(chunks))
+        sub = -(-int(max_segment_elems) // self.chunks) + max(wspec.bucket, gspec.bucket)
+        self.comms = [QSDPComm(sub, wspec, gspec, group=group, device=device) for _ in range(2)]
+        self.device = self.comms[0].device
+        self.rank = self.comms[0].rank
+        self.streams = [torch.cuda.current_stream(self.device), torch.cuda.Stream(device=self.device)]
+        self.wspec, self.gspec = wspec, gspec
+
+    def set_step_source(self, counter):
+        for c in self.comms:
+            c.set_step_source(counter)
+
+    def _run(self, fn):
+        main = torch.cuda.current_stream(self.device)
+        side = self.streams[1]
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)
+        for j in range(self.chunks):
+            with torch.cuda.stream(main if j % 2 == 0 else side):
+                fn(j, self.comms[j % 2])
+        main.wait_stream(side)
+
+    def all_gather(self, shard: torch.Tensor, segs, key: SegmentKey, out: torch.Tensor) -> torch.Tensor:
+        parts = split_segments(segs, self.wspec.bucket, self.chunks)
+        base = segs[0][0]
+        s_me = segs[self.rank][0]
+
+        def one(j, comm):
+            sub = parts[j]
+            o0 = sub[0][0] - base
+            sh = shard[sub[self.rank][0] - s_me: sub[self.rank][0] - s_me + sub[self.rank][1]]
+            comm.all_gather(sh, sub, key, out[o0:])
+        self._run(one)
+        return out
+
+    def reduce_scatter(self, full_grad: torch.Tensor, segs, key: SegmentKey, out: torch.Tensor) -> torch.Tensor:
+        parts = split_segments(segs, self.gspec.bucket, self.chunks)
+        base = segs[0][0]
+        s_me = segs[self.rank][0]
+
+        def one(j, comm):
+            sub = parts[j]
+            g0 = sub[0][0] - base
+            o = out[sub[self.rank][0] - s_me:]
+            comm.reduce_scatter(full_grad[g0:], sub, key, o)
+        self._run(one)
+        return out
+
+    def close(self):
+        for c in self.comms:
+            c.close()

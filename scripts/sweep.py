@@ -20,7 +20,7 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2302_02390_b200.comm import QSDPComm, plan_segments  # noqa: E402
+from paper_2302_02390_b200.comm import PipelinedComm, QSDPComm, plan_segments  # noqa: E402
 from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey, advance_counter  # noqa: E402
 
 HBM, NVL = 6555.2e9, 900e9
@@ -46,8 +46,10 @@ def main():
         full = torch.empty(n, device=dev)
         shard = torch.empty(max(ns, 1), device=dev)
         for bits in (8, 4):
-            comm = QSDPComm(max(m for _, m in segs), QuantSpec(bits, S, "shift"), QuantSpec(bits, S, "uniform_stochastic"),
-                            device=dev)
+            pipe = int(os.environ.get("PIPE", "0"))  # >1: PipelinedComm with this many chunks
+            ctor = (lambda *a, **k: PipelinedComm(*a, chunks=pipe, **k)) if pipe > 1 else QSDPComm
+            comm = ctor(max(m for _, m in segs), QuantSpec(bits, S, "shift"), QuantSpec(bits, S, "uniform_stochastic"),
+                        device=dev)
             comm.set_step_source(ctr)
             c = bits / 8 + 12 / S
             for kind in ("allgather", "reducescatter"):
@@ -87,7 +89,7 @@ def main():
                 nvl = c * (P - 1) / P
                 tstar = max(hbm * n / HBM, nvl * n / NVL)
                 if rank == 0:
-                    print(json.dumps({"P": P, "n": n, "mb_fp32": n * 4 / 2 ** 20, "bits": bits, "collective": kind,
+                    print(json.dumps({"P": P, "pipe": pipe, "n": n, "mb_fp32": n * 4 / 2 ** 20, "bits": bits, "collective": kind,
                                       "us": round(T * 1e6, 2), "eff_gbs": round(4 * n / T / 1e9, 1),
                                       "roofline_eff_gbs": round(4 * n / tstar / 1e9, 1),
                                       "frac_of_roofline": round(tstar / T, 3)}), flush=True)

@@ -99,6 +99,7 @@ def main():
         comm.close()
     failures += levels_all_gather(rank, world, dev)
     failures += lattice_reduce_scatter(rank, world, dev)
+    failures += pipelined(rank, world, dev)
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)
     if rank == 0:
@@ -158,6 +159,33 @@ def lattice_reduce_scatter(rank, world, dev):
             fails += 1
             print(f"rank {rank} lattice step {step}: mismatch", flush=True)
     comm.close()
+    return fails
+
+
+def pipelined(rank, world, dev):
+    """PipelinedComm (bucket-aligned sub-collectives on two comms / streams) equals one QSDPComm call."""
+    from paper_2302_02390_b200.comm import PipelinedComm
+    fails = 0
+    for size, bucket, chunks in [(3 * 1024 * 1024 + 5, 1024, 4), (200003, 256, 3)]:
+        segs = plan_segments(size, world, bucket)
+        ms = max(n for _, n in segs)
+        ws, gs = QuantSpec(8, bucket, "shift"), QuantSpec(4, bucket, "uniform_stochastic")
+        one, pipe = QSDPComm(ms, ws, gs), PipelinedComm(ms, ws, gs, chunks=chunks)
+        full = torch.randn(size, device=dev) * 0.02
+        g = torch.randn(size, device=dev) * 1e-3
+        s, n = segs[rank]
+        a, b = torch.empty(size, device=dev), torch.empty(size, device=dev)
+        one.all_gather(full[s:s + n], segs, SegmentKey(1, 2, 3, 0, 0), a)
+        pipe.all_gather(full[s:s + n], segs, SegmentKey(1, 2, 3, 0, 0), b)
+        ra, rb = torch.empty(max(n, 1), device=dev), torch.empty(max(n, 1), device=dev)
+        one.reduce_scatter(g, segs, SegmentKey(1, 2, 3, 2, rank), ra)
+        pipe.reduce_scatter(g, segs, SegmentKey(1, 2, 3, 2, rank), rb)
+        torch.cuda.synchronize()
+        if not (torch.equal(a, b) and torch.equal(ra[:n], rb[:n])):
+            fails += 1
+            print(f"rank {rank} pipelined size {size}: mismatch", flush=True)
+        one.close()
+        pipe.close()
     return fails
 
 
