@@ -251,6 +251,9 @@ qsdp_status qsdp_comm_set_step_source(qsdp_comm* c, const uint64_t* d_step);
 /* Learned weight levels for the all-gather (w.inner == QSDP_INNER_LEVELS): a
  * device float64[2^w.bits] table that stays valid while the comm uses it. */
 qsdp_status qsdp_comm_set_weight_levels(qsdp_comm* c, const double* d_levels, int32_t nlevels);
+/* Size the collectives' grids for at most `sms` SMs (0 = all): leaves the rest of the
+ * GPU to compute kernels that run concurrently (FSDP2 overlaps comm streams with compute). */
+qsdp_status qsdp_comm_set_sm_budget(qsdp_comm* c, int32_t sms);
 qsdp_status qsdp_comm_set_fused(qsdp_comm* c, int32_t enable);
 /* Quantized all-gather (ShardedMLP._gather): this rank's shard = segs[rank];
  * every rank writes the dequantized full tensor (sum of segs lengths) to full_out.

@@ -43,6 +43,7 @@ EXPORTED_SYMBOLS = (
     "qsdp_dequantize_levels_batch", "qsdp_learn_levels", "qsdp_comm_set_weight_levels",
     "qsdp_wire_parse", "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes",
     "qsdp_unpack_codes", "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice",
+    "qsdp_comm_set_sm_budget",
 )
 
 
@@ -150,6 +151,7 @@ def lib():
     L.qsdp_comm_set_step_source.argtypes = [vp, vp]
     L.qsdp_comm_set_fused.argtypes = [vp, i32]
     L.qsdp_comm_set_weight_levels.argtypes = [vp, vp, i32]
+    L.qsdp_comm_set_sm_budget.argtypes = [vp, i32]
     L.qsdp_wire_parse.argtypes = [vp, i64, ctypes.POINTER(WireInfo)]
     L.qsdp_wire_encode_device.argtypes = [vp, vp, i64, cfgp, vp, i64, vp]
     L.qsdp_wire_decode_device.argtypes = [vp, ctypes.POINTER(WireInfo), vp, vp, vp, vp]
@@ -184,7 +186,7 @@ def lib():
                  "qsdp_quantize_levels_batch", "qsdp_dequantize_levels", "qsdp_dequantize_levels_batch",
                  "qsdp_learn_levels", "qsdp_comm_set_weight_levels", "qsdp_wire_parse",
                  "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes", "qsdp_unpack_codes",
-                 "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice"):
+                 "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice", "qsdp_comm_set_sm_budget"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib

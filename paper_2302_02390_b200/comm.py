@@ -168,6 +168,11 @@ class QSDPComm:
         self._step_src = counter  # keep alive
         _lib.check(_lib.lib().qsdp_comm_set_step_source(self._h, counter.data_ptr() if counter is not None else None))
 
+    def set_sm_budget(self, sms: int) -> None:
+        """Size this communicator's kernels for at most ``sms`` SMs (0 = the whole GPU), so
+        collectives overlapping compute on another stream leave it the other SMs."""
+        _lib.check(_lib.lib().qsdp_comm_set_sm_budget(self._h, int(sms)))
+
     def set_fused(self, enable: bool) -> None:
         """Single-launch fused collectives (opt-in; env QSDP_FUSED=1 sets the default).
         A fused collective holds a grid-wide barrier and needs every CTA resident:

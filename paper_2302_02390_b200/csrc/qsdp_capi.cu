@@ -138,6 +138,7 @@ struct DynSrc {
   const unsigned long long* parity_ptr = nullptr;  // slot parity = (*parity_ptr + adj) & 1
   int64_t parity_stride = 0;
   int32_t parity_adj = 0;
+  int32_t sm_cap = 0;    // > 0: size grids for at most this many SMs (comm SM budget)
   int32_t mirror_n = 0;  // push collectives: copy every bucket to these byte offsets too
   int64_t mirror_delta[QSDP_FUSE_MAX_WORLD - 1] = {};
 };
@@ -185,6 +186,7 @@ qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const q
   int sms = 0;
   qsdp_status st = ensure_device(sms);
   if (st != QSDP_OK) return st;
+  if (dyn.sm_cap > 0 && dyn.sm_cap < sms) sms = dyn.sm_cap;
   size_t i = 0;
   while (i < jobs.size()) {
     QJobTable tab;
@@ -268,6 +270,7 @@ qsdp_status run_dequant(const std::vector<DJobSpec>& jobs, const qsdp_qcfg* cfg,
   int sms = 0;
   qsdp_status st = ensure_device(sms);
   if (st != QSDP_OK) return st;
+  if (dyn.sm_cap > 0 && dyn.sm_cap < sms) sms = dyn.sm_cap;
   for (const DJobSpec& s : jobs)
     if (s.length > 0 && (s.nsrc < 1 || s.nsrc > 8)) return fail(QSDP_EINVAL, "nsrc must be in [1, 8]");
   size_t i = 0;
@@ -736,6 +739,7 @@ struct qsdp_comm {
   bool opened[QSDP_MAX_WORLD] = {};
   const unsigned long long* step_src = nullptr;
   bool fused = true;  // single-launch collectives when the configuration allows
+  int sm_budget = 0;                // > 0: the collectives' kernels use at most this many SMs
   const double* wlevels = nullptr;  // learned weight table (w.inner == QSDP_INNER_LEVELS)
   int wnlevels = 0;
 
@@ -815,6 +819,12 @@ qsdp_status qsdp_comm_set_weight_levels(qsdp_comm* c, const double* d_levels, in
   return QSDP_OK;
 }
 
+qsdp_status qsdp_comm_set_sm_budget(qsdp_comm* c, int32_t sms) {
+  if (c == nullptr || sms < 0) return fail(QSDP_EINVAL, "bad SM budget");
+  c->sm_budget = sms;
+  return QSDP_OK;
+}
+
 qsdp_status qsdp_comm_set_fused(qsdp_comm* c, int32_t enable) {
   if (c == nullptr) return fail(QSDP_EINVAL, "null comm");
   c->fused = enable != 0;
@@ -891,6 +901,7 @@ static qsdp_status check_segs(const qsdp_comm* c, const qsdp_segment* segs) {
 static DynSrc comm_dyn(const qsdp_comm* c, int adj) {
   DynSrc d;
   d.step_ptr = c->step_src;
+  d.sm_cap = c->sm_budget;
   if (c->world > 1) {
     d.parity_ptr = c->epoch();
     d.parity_stride = c->parity_stride();

@@ -37,7 +37,7 @@ class QSDPContext:
 
     def __init__(self, max_shard_numel: int, wspec: QuantSpec, gspec: QuantSpec, root_seed: int = 0,
                  group: dist.ProcessGroup | None = None, device: torch.device | None = None,
-                 weight_levels=None):
+                 weight_levels=None, sm_budget: int | None = None):
         self.wspec, self.gspec = wspec, gspec
         self.root_seed = root_seed
         self.group = group
@@ -52,6 +52,12 @@ class QSDPContext:
         # whose grid-wide barrier needs every CTA of the GPU resident
         self.ag.set_fused(False)
         self.rs.set_fused(False)
+        # the comm streams overlap backward / forward compute: cap their SMs
+        if sm_budget is None:
+            import os
+            sm_budget = int(os.environ.get("QSDP_SM_BUDGET", "0"))
+        self.ag.set_sm_budget(sm_budget)
+        self.rs.set_sm_budget(sm_budget)
         self.step = 0
         self.phase = PHASE_W_FWD
         self.calls = {"allgather": 0, "reducescatter": 0}
