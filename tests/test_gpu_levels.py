@@ -230,3 +230,17 @@ def test_learned_vs_uniform_error(oracle, L):
 
     assert ue == pytest.approx(rel(np.linspace(0.0, 1.0, 16)), rel=1e-12)
     assert le == pytest.approx(rel(q), rel=1e-12)
+
+
+def test_learn_levels_ties_and_clusters(oracle, L):
+    """Levels one ulp apart and values on exact midpoints: rounded-distance ties
+    (np.argmin takes the first index) and order breaks exercise the exact fallbacks."""
+    rng = np.random.default_rng(21)
+    base = np.sort(rng.uniform(0, 1, 60))
+    clus = np.array([0.5, np.nextafter(0.5, 1), np.nextafter(np.nextafter(0.5, 1), 1), 0.25])
+    q0 = np.unique(np.concatenate([base, clus]))[:64]
+    mids = (q0[:-1] + q0[1:]) / 2
+    vals = np.concatenate([mids, q0, rng.uniform(0, 1, 3000), np.full(50, 0.5), mids[::-1]])
+    for lr in (0.01, 0.5, 1.0, 1.7):
+        out = L.learn_levels(vals, L.LevelTable(q0), lr)
+        np.testing.assert_array_equal(out.levels, oracle.learn_levels(vals, q0, lr), err_msg=f"lr={lr}")
