@@ -130,6 +130,7 @@ struct QJobSpec {
   float* meta;
   SeedPrefix seed;
   uint64_t key[5];
+  void* dq_out = nullptr;  // fused dequant destination (TMA32 path only; see fdq_ok)
 };
 
 // Device-side sources that make a launch sequence replayable as a CUDA graph.
@@ -139,6 +140,8 @@ struct DynSrc {
   int64_t parity_stride = 0;
   int32_t parity_adj = 0;
   int32_t sm_cap = 0;    // > 0: size grids for at most this many SMs (comm SM budget)
+  int32_t dq_dtype = 0;  // fused dequant epilogue: output dtype and K4's single-source 0.0 + v
+  int32_t dq_add0 = 0;
   int32_t mirror_n = 0;  // push collectives: copy every bucket to these byte offsets too
   int64_t mirror_delta[QSDP_FUSE_MAX_WORLD - 1] = {};
 };
@@ -155,6 +158,8 @@ void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, co
   tab.parity_ptr = dyn.parity_ptr;
   tab.parity_stride = dyn.parity_stride;
   tab.parity_adj = dyn.parity_adj;
+  tab.dq_dtype = dyn.dq_dtype;
+  tab.dq_add0 = dyn.dq_add0;
   tab.mirror_n = dyn.mirror_n;
   for (int k = 0; k < dyn.mirror_n; ++k) tab.mirror_delta[k] = dyn.mirror_delta[k];
   int64_t nb = 0;
@@ -172,6 +177,7 @@ void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, co
     J.bucket_base = nb;
     J.seed = s.seed;
     for (int w = 0; w < 5; ++w) J.key[w] = s.key[w];
+    J.dq_out = s.dq_out;
     nb += (s.length + cfg->bucket - 1) / cfg->bucket;
     vec = vec && aligned(s.x, 16);
   }
@@ -944,6 +950,16 @@ static bool push_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
          cfg->bucket * isz <= 8192;
 }
 
+// The fused dequant epilogue lives in the TMA32 quantizer: direct widths,
+// S % 8 == 0, a whole warp per bucket (S >= 72), S * sizeof(T) <= 8 KB
+// (launch_q_t's routing), an fp32 / fp64 / bf16 output.
+static bool fdq_ok(const qsdp_qcfg* cfg, int in_dtype, int out_dtype) {
+  const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
+  const int isz = in_dtype == QSDP_F64 ? 8 : 4;
+  return cfg->inner != QSDP_INNER_LEVELS && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 72 &&
+         cfg->bucket * isz <= 8192 && (out_dtype == QSDP_F32 || out_dtype == QSDP_F64 || out_dtype == QSDP_BF16);
+}
+
 static FuseSync comm_sync(const qsdp_comm* c) {
   FuseSync fs;
   memset(&fs, 0, sizeof(fs));
@@ -1002,16 +1018,26 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
       if (p != c->rank) dq.mirror_delta[dq.mirror_n++] = (int64_t)((uintptr_t)c->peer[p] - (uintptr_t)c->base);
   std::vector<QJobSpec> q(1, comm_qjob(shard, segs[c->rank], c->slot(c->base, push ? c->rank : 0), c->slot_codes,
                                        *key, 0));  // key worker 0 (sharded.py:341)
-  std::vector<DJobSpec> d(c->world);
   const size_t osz = dtype_size(out_dtype);
+  // this rank's own shard is dequantized by the quantizer itself (fused epilogue):
+  // the dequant launch covers the peers' shards only (none at world 1)
+  const bool fdq = fdq_ok(cfg, in_dtype, out_dtype);
+  if (fdq) {
+    q[0].dq_out = static_cast<uint8_t*>(full_out) + (size_t)(segs[c->rank].global_start - segs[0].global_start) * osz;
+    dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;
+  }
+  std::vector<DJobSpec> d;
   for (int p = 0; p < c->world; ++p) {
-    memset(&d[p], 0, sizeof(DJobSpec));
+    if (fdq && p == c->rank) continue;
+    DJobSpec js;
+    memset(&js, 0, sizeof(DJobSpec));
     uint8_t* sl = push ? c->slot(c->base, p) : c->slot(c->peer[p], 0);
-    d[p].codes[0] = sl;
-    d[p].meta[0] = reinterpret_cast<const float*>(sl + c->slot_codes);
-    d[p].nsrc = 1;
-    d[p].length = segs[p].length;
-    d[p].out = static_cast<uint8_t*>(full_out) + (size_t)(segs[p].global_start - segs[0].global_start) * osz;
+    js.codes[0] = sl;
+    js.meta[0] = reinterpret_cast<const float*>(sl + c->slot_codes);
+    js.nsrc = 1;
+    js.length = segs[p].length;
+    js.out = static_cast<uint8_t*>(full_out) + (size_t)(segs[p].global_start - segs[0].global_start) * osz;
+    d.push_back(js);
   }
   if (fused_cfg_ok(c, cfg, in_dtype)) {
     bool launched = false;
@@ -1026,7 +1052,8 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
     st = comm_barrier(c, s);
     if (st != QSDP_OK) return st;
   }
-  // 3. dequantize all P shards into the gathered buffer
+  // 3. dequantize the (remaining) shards into the gathered buffer
+  if (d.empty()) return QSDP_OK;
   return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0), lv ? c->wlevels : nullptr);
 }
 
@@ -1077,8 +1104,17 @@ static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int3
     st = try_fused(c, q, d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 1), launched);
     if (st != QSDP_OK || launched) return st;
   }
-  st = run_quantize(q, in_dtype, cfg, nullptr, s, comm_dyn(c, 1));
+  DynSrc dq = comm_dyn(c, 1);
+  // world 1: the average of one source is the quantizer's own dequant epilogue (0.0 + v)
+  const bool fdq1 = c->world == 1 && lat == nullptr && shard_out != nullptr && fdq_ok(cfg, in_dtype, out_dtype);
+  if (fdq1) {
+    q[0].dq_out = shard_out;
+    dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;
+    dq.dq_add0 = 1;
+  }
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
   if (st != QSDP_OK) return st;
+  if (fdq1) return QSDP_OK;
   if (c->world > 1) {
     st = comm_barrier(c, s);
     if (st != QSDP_OK) return st;

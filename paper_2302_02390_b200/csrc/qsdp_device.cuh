@@ -197,6 +197,7 @@ struct QJob {
   int64_t bucket_base;    // prefix: global bucket index of this job's bucket 0
   SeedPrefix seed;        // root, step, layer, phase, worker already absorbed (static step)
   uint64_t key[5];        // raw (root, step, layer, phase, worker) for a device step source
+  void* dq_out;           // fused dequant of this segment (element 0), or nullptr (TMA32 path only)
 };
 
 struct QJobTable {
@@ -218,6 +219,10 @@ struct QJobTable {
   // (its address + mirror_delta[k]) -- the same slot in a peer's workspace
   int32_t mirror_n;
   int64_t mirror_delta[QSDP_FUSE_MAX_WORLD - 1];
+  // fused dequant epilogue (jobs with dq_out): K3's value (lo + code*pitch) + shift,
+  // or K4's single-source 0.0 + value (dq_add0), stored as dq_dtype (0 f32, 1 f64, 2 bf16)
+  int32_t dq_dtype;
+  int32_t dq_add0;
 };
 
 struct DJob {

@@ -546,16 +546,116 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
 //    fq in {d_hi, d_hi+1} or fq == 0 off the bucket's extrema; those elements
 //    are recomputed with the exact __ddiv_rn chain.
 // ---------------------------------------------------------------------------
+// COH: codes written earlier in the same launch (fused collectives) or by a
+// peer -- read at L2 (ld.global.cg), never through the non-coherent path.
+template <int BITS, bool COH = false>
+__device__ __forceinline__ uint64_t load_group_direct(const uint8_t* __restrict__ p, int gi) {
+  if constexpr (COH) {
+    if (BITS == 8) return __ldcg(reinterpret_cast<const unsigned int*>(p) + gi);
+    if (BITS == 4) return __ldcg(reinterpret_cast<const unsigned short*>(p) + gi);
+    if (BITS == 16) return __ldcg(reinterpret_cast<const unsigned long long*>(p) + gi);
+    return __ldcg(reinterpret_cast<const unsigned char*>(p) + gi);
+  } else {
+    if (BITS == 8) return __ldg(reinterpret_cast<const uint32_t*>(p) + gi);
+    if (BITS == 4) return __ldg(reinterpret_cast<const uint16_t*>(p) + gi);
+    if (BITS == 16) return __ldg(reinterpret_cast<const unsigned long long*>(p) + gi);
+    return __ldg(p + gi);
+  }
+}
+
+__device__ __forceinline__ double code_to_double(uint32_t c) {
+  // exact: 2^52 + c reinterpreted, minus 2^52
+  return __dsub_rn(__longlong_as_double(0x4330000000000000ll | (long long)c), 4503599627370496.0);
+}
+
+template <int OUT, bool VEC>
+__device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, const double acc[4]) {
+  if (OUT == 0) {
+    float* o = reinterpret_cast<float*>(out) + idx;
+    const float4 f = make_float4(__double2float_rn(acc[0]), __double2float_rn(acc[1]), __double2float_rn(acc[2]),
+                                 __double2float_rn(acc[3]));
+    if (VEC && n_left >= 4) {
+      *reinterpret_cast<float4*>(o) = f;
+    } else {
+      const float fv[4] = {f.x, f.y, f.z, f.w};
+      for (int i = 0; i < 4 && i < n_left; ++i) o[i] = fv[i];
+    }
+  } else if (OUT == 1) {
+    double* o = reinterpret_cast<double*>(out) + idx;
+    if (VEC && n_left >= 4) {
+      reinterpret_cast<double2*>(o)[0] = make_double2(acc[0], acc[1]);
+      reinterpret_cast<double2*>(o)[1] = make_double2(acc[2], acc[3]);
+    } else {
+      for (int i = 0; i < 4 && i < n_left; ++i) o[i] = acc[i];
+    }
+  } else {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + idx;
+    __nv_bfloat16 h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __float2bfloat16_rn(__double2float_rn(acc[i]));
+    if (VEC && n_left >= 4) {
+      uint2 u;
+      u.x = (uint32_t)__bfloat16_as_ushort(h[0]) | ((uint32_t)__bfloat16_as_ushort(h[1]) << 16);
+      u.y = (uint32_t)__bfloat16_as_ushort(h[2]) | ((uint32_t)__bfloat16_as_ushort(h[3]) << 16);
+      *reinterpret_cast<uint2*>(o) = u;
+    } else {
+      for (int i = 0; i < 4 && i < n_left; ++i) o[i] = h[i];
+    }
+  }
+}
+
+// Fused dequant (the collective's own shard; world 1: the whole collective):
+// the quantizer dequantizes its codes while they are in registers, exactly as
+// K3 (or K4 with one source) would: v = (lo + code*pitch) + shift in fp64
+// (quantize.py:209-232), K4: 0.0 + v (sharded.py:385-431, divisor 1).  The
+// dequant launch and the code read-back from HBM disappear.
+struct FusedDq {
+  void* out;  // element 0 of the bucket, or nullptr
+  double lo, pitch, shift;
+  int dtype, add0;
+};
+template <int BITS>
+__device__ __forceinline__ void dq_emit4(const FusedDq& f, int e, int n_left, uint64_t w) {
+  double v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double c = code_to_double((uint32_t)((w >> (i * BITS)) & ((1ull << BITS) - 1ull)));
+    v[i] = __dadd_rn(__dadd_rn(f.lo, __dmul_rn(c, f.pitch)), f.shift);
+    if (f.add0) v[i] = __dadd_rn(0.0, v[i]);
+  }
+  if (f.dtype == 0) store_out4<0, true>(f.out, e, n_left, v);
+  else if (f.dtype == 1) store_out4<1, true>(f.out, e, n_left, v);
+  else store_out4<2, true>(f.out, e, n_left, v);
+}
+template <bool FDQ>
+__device__ __forceinline__ FusedDq fused_dq(const QJobTable& tab, const QJob& J, int64_t off, float lof, float hif,
+                                            float shift_f, int bits) {
+  FusedDq f;
+  f.out = nullptr;
+  f.lo = f.pitch = f.shift = 0.0;
+  f.dtype = tab.dq_dtype;
+  f.add0 = tab.dq_add0;
+  if (FDQ && J.dq_out != nullptr) {
+    f.out = static_cast<uint8_t*>(J.dq_out) + off * (tab.dq_dtype == 1 ? 8 : tab.dq_dtype == 2 ? 2 : 4);
+    f.lo = (double)lof;
+    f.pitch = __ddiv_rn(__dsub_rn((double)hif, f.lo), (double)((1u << bits) - 1u));  // QuantizedBlock.pitch
+    f.shift = (double)shift_f;
+  }
+  return f;
+}
+
 // Partial / unaligned / degenerate bucket (one per segment at most on the hot
 // path): per-lane seeding and the Coder path; out of line to keep the fast
 // loop's register budget.  Returns the bucket's f32 shift.
-template <typename T, int INNER, int BITS>
+template <typename T, int INNER, int BITS, bool FDQ = false>
 static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix& seed, uint64_t start, const T* x, int n,
                                                              int gl, uint8_t* cbase, float lof, float hif,
-                                                             bool degenerate, int lane) {
+                                                             bool degenerate, int lane, const QJobTable& tab,
+                                                             const QJob& J, int64_t off) {
   Coder<T, INNER> cd;
   float shift_f = 0.0f;
   if (!degenerate) cd.setup(lof, hif, BITS, seed, start, lane, 32, shift_f);
+  const FusedDq fq = fused_dq<FDQ>(tab, J, off, lof, hif, degenerate ? 0.0f : shift_f, BITS);
   const int64_t pb = payload_bytes(n, BITS);
   for (int g = 0; g < gl; ++g) {
     const int gi = g * 32 + lane;
@@ -568,6 +668,7 @@ static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix
         w = cd.group(v, e, n, BITS);
       }
       store_direct<BITS>(cbase, gi, w, pb, e + 4 <= n);
+      if (fq.out != nullptr) dq_emit4<BITS>(fq, e, n - e, w);
     }
   }
   return shift_f;
@@ -677,7 +778,7 @@ struct JobCursor {
   }
 };
 
-template <typename T, int INNER, int BITS, int NST>
+template <typename T, int INNER, int BITS, int NST, bool FDQ = false>
 __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_t* smem) {
   const int64_t poff = q_parity_off(tab);
   using Tr = InTraits<T>;
@@ -810,6 +911,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
       const double K1 = __dmul_rn(inv, top);
       if (INNER == 0) {
         shift_f = __double2float_rn(__dmul_rn(r, span));  // _f32(r*(hi-lo))
+        const FusedDq fq4 = fused_dq<FDQ>(tab, J, br.off, lof, hif, shift_f, BITS);
         const double C = __dsub_rn(kMagic + 0.5, __dmul_rn(r, top));
         // A certified code lies in [0, top]: the low 19 integer bits are the code.
         auto code4 = [&](const T v[4], uint32_t c[4]) -> bool {
@@ -838,7 +940,9 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             lds_group(sb, 4 * gi, v);
             uint32_t c[4];
             if (code4(v, c)) fix4(v, c);
-            store_direct<BITS>(cbase, gi, pack4<BITS>(c[0], c[1], c[2], c[3]), 0, true);
+            const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
+            store_direct<BITS>(cbase, gi, w, 0, true);
+            if (fq4.out != nullptr) dq_emit4<BITS>(fq4, 4 * gi, 4, w);
           }
         } else {
           for (int g = 0; g < gl; ++g) {
@@ -849,7 +953,9 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
               lds_group(sb, e, v);
               uint32_t c[4];
               if (code4(v, c)) fix4(v, c);
-              store_direct<BITS>(cbase, gi, pack4<BITS>(c[0], c[1], c[2], c[3]), 0, true);
+              const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
+              store_direct<BITS>(cbase, gi, w, 0, true);
+              if (fq4.out != nullptr) dq_emit4<BITS>(fq4, e, n - e, w);
             }
           }
         }
@@ -863,6 +969,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
         const JumpEntry oj = g_jump[8 * 32 - 7];
         const U128 OJa = oj.a;
         const U128 jc = mul128(oj.g, inc);
+        const FusedDq fqs = fused_dq<FDQ>(tab, J, br.off, lof, hif, 0.0f, BITS);
         const int ol = S / 256;
         for (int g = 0; g < ol; ++g) {
           const int o = g * 32 + lane;
@@ -886,6 +993,10 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
           }
           if (unc) w = stoch_octet_exact<T, BITS>(sb + 8 * o, st0, inc, lo, span, K1, top);
           store_octet<BITS>(cbase, o, w);
+          if (fqs.out != nullptr) {
+            dq_emit4<BITS>(fqs, 8 * o, 4, w);
+            dq_emit4<BITS>(fqs, 8 * o + 4, 4, w >> (4 * BITS));
+          }
           st = add128(mul128(OJa, st), jc);
         }
         }
@@ -895,6 +1006,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
         const JumpEntry ej = g_jump[4 * 32 - 3];
         const U128 JA = ej.a;
         const U128 jc = mul128(ej.g, inc);
+        const FusedDq fqq = fused_dq<FDQ>(tab, J, br.off, lof, hif, 0.0f, BITS);
 #pragma unroll 2
         for (int g = 0; g < gl; ++g) {
           const int gi = g * 32 + lane;
@@ -919,12 +1031,13 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             }
             st = add128(mul128(JA, st), jc);
             store_direct<BITS>(cbase, gi, w, 0, true);
+            if (fqq.out != nullptr) dq_emit4<BITS>(fqq, e, n - e, w);
           }
         }
       }
     } else if (n > 0) {
-      shift_f = quantize_bucket_general<T, INNER, BITS>(q_seed(tab, J), (uint64_t)(J.global_start + br.off), in_smem ? sb : gx,
-                                                        n, gl, cbase, lof, hif, degenerate, lane);
+      shift_f = quantize_bucket_general<T, INNER, BITS, FDQ>(q_seed(tab, J), (uint64_t)(J.global_start + br.off), in_smem ? sb : gx,
+                                                        n, gl, cbase, lof, hif, degenerate, lane, tab, J, br.off);
     }
     if (lane == 0) {
       float* m = meta_at(J.meta, poff) + 3 * br.lb;
@@ -939,10 +1052,10 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
   }
 }
 
-template <typename T, int INNER, int BITS, int NST>
+template <typename T, int INNER, int BITS, int NST, bool FDQ = false>
 __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_constant__ QJobTable tab) {
   extern __shared__ __align__(128) uint8_t smem[];
-  quantize_tma32_body<T, INNER, BITS, NST>(tab, smem);
+  quantize_tma32_body<T, INNER, BITS, NST, FDQ>(tab, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1177,63 +1290,6 @@ __device__ __forceinline__ uint64_t load_group_bits_any(const uint8_t* p, int gi
   return bits == 16 ? v : (v & ((1ull << (4 * bits)) - 1ull));
 }
 
-// COH: codes written earlier in the same launch (fused collectives) or by a
-// peer -- read at L2 (ld.global.cg), never through the non-coherent path.
-template <int BITS, bool COH = false>
-__device__ __forceinline__ uint64_t load_group_direct(const uint8_t* __restrict__ p, int gi) {
-  if constexpr (COH) {
-    if (BITS == 8) return __ldcg(reinterpret_cast<const unsigned int*>(p) + gi);
-    if (BITS == 4) return __ldcg(reinterpret_cast<const unsigned short*>(p) + gi);
-    if (BITS == 16) return __ldcg(reinterpret_cast<const unsigned long long*>(p) + gi);
-    return __ldcg(reinterpret_cast<const unsigned char*>(p) + gi);
-  } else {
-    if (BITS == 8) return __ldg(reinterpret_cast<const uint32_t*>(p) + gi);
-    if (BITS == 4) return __ldg(reinterpret_cast<const uint16_t*>(p) + gi);
-    if (BITS == 16) return __ldg(reinterpret_cast<const unsigned long long*>(p) + gi);
-    return __ldg(p + gi);
-  }
-}
-
-__device__ __forceinline__ double code_to_double(uint32_t c) {
-  // exact: 2^52 + c reinterpreted, minus 2^52
-  return __dsub_rn(__longlong_as_double(0x4330000000000000ll | (long long)c), 4503599627370496.0);
-}
-
-template <int OUT, bool VEC>
-__device__ __forceinline__ void store_out4(void* out, int64_t idx, int n_left, const double acc[4]) {
-  if (OUT == 0) {
-    float* o = reinterpret_cast<float*>(out) + idx;
-    const float4 f = make_float4(__double2float_rn(acc[0]), __double2float_rn(acc[1]), __double2float_rn(acc[2]),
-                                 __double2float_rn(acc[3]));
-    if (VEC && n_left >= 4) {
-      *reinterpret_cast<float4*>(o) = f;
-    } else {
-      const float fv[4] = {f.x, f.y, f.z, f.w};
-      for (int i = 0; i < 4 && i < n_left; ++i) o[i] = fv[i];
-    }
-  } else if (OUT == 1) {
-    double* o = reinterpret_cast<double*>(out) + idx;
-    if (VEC && n_left >= 4) {
-      reinterpret_cast<double2*>(o)[0] = make_double2(acc[0], acc[1]);
-      reinterpret_cast<double2*>(o)[1] = make_double2(acc[2], acc[3]);
-    } else {
-      for (int i = 0; i < 4 && i < n_left; ++i) o[i] = acc[i];
-    }
-  } else {
-    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + idx;
-    __nv_bfloat16 h[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) h[i] = __float2bfloat16_rn(__double2float_rn(acc[i]));
-    if (VEC && n_left >= 4) {
-      uint2 u;
-      u.x = (uint32_t)__bfloat16_as_ushort(h[0]) | ((uint32_t)__bfloat16_as_ushort(h[1]) << 16);
-      u.y = (uint32_t)__bfloat16_as_ushort(h[2]) | ((uint32_t)__bfloat16_as_ushort(h[3]) << 16);
-      *reinterpret_cast<uint2*>(o) = u;
-    } else {
-      for (int i = 0; i < 4 && i < n_left; ++i) o[i] = h[i];
-    }
-  }
-}
 
 // The lattice shift of this call: r = sample_shift(d, bucket_rng(key..., 0))
 // = -d/2 + d * random() (quantize.py:130-132, numpy's unfused uniform).
@@ -1822,7 +1878,7 @@ __global__ void __launch_bounds__(256, 2) fused_collective_kernel(const __grid_c
                                                                   const __grid_constant__ FuseSync fs) {
   extern __shared__ __align__(128) uint8_t smem[];
   const unsigned long long target = ld_dev_u64(fs.epoch) + 1ull;
-  quantize_tma32_body<T, INNER, BITS, NST>(qt, smem);
+  quantize_tma32_body<T, INNER, BITS, NST, true>(qt, smem);
   fused_barrier(fs, target);
   // the phase-A ring is free again: reuse its start for the per-source scale rows
   dequant_body<BITS, 32, OUT, true, ACC, true>(dt, reinterpret_cast<double*>(smem));
@@ -1864,15 +1920,15 @@ inline int persistent_grid(F kern, int threads, size_t smem, int64_t total_bucke
 }
 
 // Fast TMA path.  Returns false when the configuration needs the general kernel.
-template <typename T, int INNER, int BITS>
-cudaError_t launch_q_tma32(const QJobTable& tab, int sms, cudaStream_t s) {
+template <typename T, int INNER, int BITS, bool FDQ>
+cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
   constexpr int NST = 2;
   const size_t stage = (size_t)tab.bucket * sizeof(T);
   int wpc = 8;
   while (wpc > 2 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
   const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t) +
                       (size_t)wpc * 32 * sizeof(SeedOut);
-  auto kern = quantize_tma32_kernel<T, INNER, BITS, NST>;
+  auto kern = quantize_tma32_kernel<T, INNER, BITS, NST, FDQ>;
   static thread_local size_t smem_set = 0;  // per instantiation: set once, not during graph capture
   if (smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1882,6 +1938,14 @@ cudaError_t launch_q_tma32(const QJobTable& tab, int sms, cudaStream_t s) {
   const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, 1, sms);
   kern<<<grid, wpc * 32, smem, s>>>(tab);
   return cudaGetLastError();
+}
+
+// Fast TMA path; the fused-dequant variant only when a job asks for it.
+template <typename T, int INNER, int BITS>
+cudaError_t launch_q_tma32(const QJobTable& tab, int sms, cudaStream_t s) {
+  bool fdq = false;
+  for (int j = 0; j < tab.njobs; ++j) fdq = fdq || tab.jobs[j].dq_out != nullptr;
+  return fdq ? launch_q_tma32_v<T, INNER, BITS, true>(tab, sms, s) : launch_q_tma32_v<T, INNER, BITS, false>(tab, sms, s);
 }
 
 template <typename T, int INNER, int BITS, int TL>
