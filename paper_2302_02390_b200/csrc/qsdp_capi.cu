@@ -142,6 +142,7 @@ struct DynSrc {
   int32_t sm_cap = 0;    // > 0: size grids for at most this many SMs (comm SM budget)
   int32_t dq_dtype = 0;  // fused dequant epilogue: output dtype and K4's single-source 0.0 + v
   int32_t dq_add0 = 0;
+  int32_t dq_nocodes = 0;  // world 1: nobody reads the codes
   int32_t mirror_n = 0;  // push collectives: copy every bucket to these byte offsets too
   int64_t mirror_delta[QSDP_FUSE_MAX_WORLD - 1] = {};
 };
@@ -160,6 +161,7 @@ void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, co
   tab.parity_adj = dyn.parity_adj;
   tab.dq_dtype = dyn.dq_dtype;
   tab.dq_add0 = dyn.dq_add0;
+  tab.dq_nocodes = dyn.dq_nocodes;
   tab.mirror_n = dyn.mirror_n;
   for (int k = 0; k < dyn.mirror_n; ++k) tab.mirror_delta[k] = dyn.mirror_delta[k];
   int64_t nb = 0;
@@ -1025,6 +1027,7 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
   if (fdq) {
     q[0].dq_out = static_cast<uint8_t*>(full_out) + (size_t)(segs[c->rank].global_start - segs[0].global_start) * osz;
     dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;
+    dq.dq_nocodes = c->world == 1 ? 1 : 0;  // world 1: the fused dequant is the only reader
   }
   std::vector<DJobSpec> d;
   for (int p = 0; p < c->world; ++p) {
@@ -1111,6 +1114,7 @@ static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int3
     q[0].dq_out = shard_out;
     dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;
     dq.dq_add0 = 1;
+    dq.dq_nocodes = 1;
   }
   st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
   if (st != QSDP_OK) return st;

@@ -223,6 +223,8 @@ struct QJobTable {
   // or K4's single-source 0.0 + value (dq_add0), stored as dq_dtype (0 f32, 1 f64, 2 bf16)
   int32_t dq_dtype;
   int32_t dq_add0;
+  int32_t dq_nocodes;  // world 1: the fused dequant is the only consumer -> codes not stored
+  int32_t _pad_dq;
 };
 
 struct DJob {

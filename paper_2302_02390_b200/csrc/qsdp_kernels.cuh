@@ -667,7 +667,7 @@ static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix
         load_group<T, false, false>(x, e, n, v);
         w = cd.group(v, e, n, BITS);
       }
-      store_direct<BITS>(cbase, gi, w, pb, e + 4 <= n);
+      if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, pb, e + 4 <= n);
       if (fq.out != nullptr) dq_emit4<BITS>(fq, e, n - e, w);
     }
   }
@@ -941,7 +941,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             uint32_t c[4];
             if (code4(v, c)) fix4(v, c);
             const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
-            store_direct<BITS>(cbase, gi, w, 0, true);
+            if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
             if (fq4.out != nullptr) dq_emit4<BITS>(fq4, 4 * gi, 4, w);
           }
         } else {
@@ -954,7 +954,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
               uint32_t c[4];
               if (code4(v, c)) fix4(v, c);
               const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
-              store_direct<BITS>(cbase, gi, w, 0, true);
+              if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
               if (fq4.out != nullptr) dq_emit4<BITS>(fq4, e, n - e, w);
             }
           }
@@ -992,7 +992,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             if (i < 7) st = pcg_step(st, inc);
           }
           if (unc) w = stoch_octet_exact<T, BITS>(sb + 8 * o, st0, inc, lo, span, K1, top);
-          store_octet<BITS>(cbase, o, w);
+          if (!FDQ || !tab.dq_nocodes) store_octet<BITS>(cbase, o, w);
           if (fqs.out != nullptr) {
             dq_emit4<BITS>(fqs, 8 * o, 4, w);
             dq_emit4<BITS>(fqs, 8 * o + 4, 4, w >> (4 * BITS));
@@ -1030,7 +1030,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
               if (i < 3) st = pcg_step(st, inc);
             }
             st = add128(mul128(JA, st), jc);
-            store_direct<BITS>(cbase, gi, w, 0, true);
+            if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
             if (fqq.out != nullptr) dq_emit4<BITS>(fqq, e, n - e, w);
           }
         }
