@@ -98,6 +98,30 @@ struct InTraits<double> {
   static constexpr Key kPosInf = 0x7ff0000000000000ll, kNegInf = (long long)0x800fffffffffffffull;
 };
 
+// NaN-propagating 3-input min/max (FMNMX3.NAN) and warp reductions (CREDUX.*.F32.NAN), sm_100a.
+// A NaN anywhere makes the result NaN, an infinity reaches the extremum, so the reduced pair alone
+// says whether the bucket is finite.  The sign of a zero extremum is left to the key path.
+__device__ __forceinline__ float fmin3_nan(float a, float b, float c) {
+  float d;
+  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float fmax3_nan(float a, float b, float c) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float warp_min_nan(float a) {
+  float d;
+  asm volatile("redux.sync.min.NaN.f32 %0, %1, 0xffffffff;" : "=f"(d) : "f"(a));
+  return d;
+}
+__device__ __forceinline__ float warp_max_nan(float a) {
+  float d;
+  asm volatile("redux.sync.max.NaN.f32 %0, %1, 0xffffffff;" : "=f"(d) : "f"(a));
+  return d;
+}
+
 // Streaming 128-bit loads (no L1 allocation) when a value is read once;
 // cached loads when the bucket is re-read in a second pass.
 template <bool STREAM>
@@ -855,11 +879,31 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
     };
     if (in_smem && (S & 127) == 0) {
       const int gfull = S >> 7;
+      bool keyed = true;
+      if constexpr (sizeof(T) == 4) {
+        // float min/max (1 FMNMX3 per 2 elements and bound), keys only for a zero extremum
+        float mnf = __int_as_float(0x7f800000), mxf = __int_as_float(0xff800000);
 #pragma unroll 4
-      for (int g = 0; g < gfull; ++g) {
-        T v[4];
-        lds_group(sb, 4 * (g * 32 + lane), v);
-        keys4(v);
+        for (int g = 0; g < gfull; ++g) {
+          T v[4];
+          lds_group(sb, 4 * (g * 32 + lane), v);
+          mnf = fmin3_nan(fmin3_nan(mnf, v[0], v[1]), v[2], v[3]);
+          mxf = fmax3_nan(fmax3_nan(mxf, v[0], v[1]), v[2], v[3]);
+        }
+        mnf = warp_min_nan(mnf);
+        mxf = warp_max_nan(mxf);
+        keyed = mnf == 0.0f || mxf == 0.0f;  // -0 vs +0: total order on keys
+        mnk = Tr::key(mnf);
+        mxk = Tr::key(mxf);
+        if (keyed) mnk = Tr::kMax, mxk = Tr::kMin;
+      }
+      if (keyed) {
+#pragma unroll 4
+        for (int g = 0; g < gfull; ++g) {
+          T v[4];
+          lds_group(sb, 4 * (g * 32 + lane), v);
+          keys4(v);
+        }
       }
     } else if (in_smem) {
       for (int g = 0; g < gl; ++g) {
@@ -931,6 +975,24 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
 #pragma unroll
           for (int i = 0; i < 4; ++i) c[i] = exact_shift_code(__dsub_rn(Tr::to_d(v[i]), lo), span, r, pitch, top);
         };
+        // fp32 certificate (float input, b <= 8, span in [2^-100, 2^100]):
+        // t = fl(fl(fl(v-lo)*K1f + Cf) + 1536) with Cf = fl(1/2 - r*top + 2^-13) keeps 13 fraction
+        // bits and |t - 1536 - 2^-13 - y| < 0.875 * 2^-13, so floor(t) - 1536 is the code unless t's
+        // fraction is 0 or 1 units; those groups take the fp64 path above.
+        const bool f32ok = sizeof(T) == 4 && BITS <= 8 && span >= 0x1p-100 && span <= 0x1p100;
+        const float K1f = __double2float_rn(K1);
+        const float Cf = __double2float_rn(__dadd_rn(__dsub_rn(0.5, __dmul_rn(r, top)), 0x1p-13));
+        auto code4f = [&](const T v[4], uint32_t c[4]) -> bool {
+          uint32_t m = 0xffffffffu;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float a = __fsub_rn((float)v[i], lof);
+            const uint32_t b = __float_as_uint(__fadd_rn(__fmaf_rn(a, K1f, Cf), 1536.0f));
+            m = min(m, b & 0x1ffeu);
+            c[i] = BITS == 8 ? b >> 13 : (b >> 13) & TOP;  // pack4<8> takes the low byte
+          }
+          return m == 0u;
+        };
         if ((S & 127) == 0) {  // every lane owns exactly S/128 full groups
           const int gfull = S >> 7;
 #pragma unroll 2
@@ -939,7 +1001,11 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             T v[4];
             lds_group(sb, 4 * gi, v);
             uint32_t c[4];
-            if (code4(v, c)) fix4(v, c);
+            if (f32ok) {
+              if (code4f(v, c) && code4(v, c)) fix4(v, c);
+            } else if (code4(v, c)) {
+              fix4(v, c);
+            }
             const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
             if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
             if (fq4.out != nullptr) dq_emit4<BITS>(fq4, 4 * gi, 4, w);

@@ -73,6 +73,36 @@ def test_large_segment_vs_oracle(oracle, inner, bits):
     assert mism.size == 0, f"{mism.size} code bytes differ, first at {mism[:5]}"
 
 
+@pytest.mark.parametrize("bits", [8, 4, 2, 1])
+def test_shift_fp32_certificate_stress(oracle, bits):
+    """K1's fp32-certified fast path against the oracle on 2^21 elements per
+    distribution: grid-valued data (many exact ties), tiny and huge spans on both sides of the
+    fp32 guard, zero extrema of either sign, subnormals."""
+    rng = np.random.default_rng(bits)
+    n = 1 << 21
+    dists = {
+        "grid": np.floor(rng.uniform(0, 256, n)) / 255.0,
+        "uniform": rng.uniform(-1, 1, n),
+        "tiny_span": 1.0 + rng.uniform(0, 1, n) * 2.0 ** -20,
+        "subnormal": rng.uniform(0, 1, n) * 1e-40,
+        "span_near_guard": rng.uniform(-1, 1, n) * 2.0 ** 99,
+        "span_beyond_guard": rng.uniform(-1, 1, n) * 2.0 ** 120,
+        "small_beyond_guard": rng.uniform(0, 1, n) * 2.0 ** -110,
+        "zero_extrema": np.where(rng.uniform(size=n) < 0.5, rng.uniform(0, 1, n), 0.0) *
+                        np.where(np.arange(n) % 2048 < 1024, 1.0, -1.0),
+    }
+    dists["zero_extrema"][::7] = -0.0
+    for name, x in dists.items():
+        x = x.astype(np.float32)
+        key = (3, 1, 4, 1, 5)
+        spec = QuantSpec(bits, 1024, "shift")
+        codes, meta = _q(x, 12345, spec, key)
+        oc, om, _ = oracle.quantize_segment(x, 12345, 1024, bits, 0, key, 8)
+        mism = np.flatnonzero(codes != oc)
+        assert mism.size == 0, (name, mism.size, mism[:5])
+        assert np.array_equal(meta, om), name
+
+
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_edge_lengths_and_alignment(oracle, dtype):
     """Short / empty-ish segments, misaligned starts (scalar path), odd buckets (generic path)."""
