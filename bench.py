@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--out-dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--check-e2e", action="store_true", help="verify the e2e step's results once")
     ap.add_argument("--no-gpt", action="store_true")
     ap.add_argument("--no-levels", action="store_true", help="skip the learned-levels kernel timings")
     ap.add_argument("--serial", action="store_true",
@@ -542,6 +543,14 @@ def main():
         bi = sum(h["shard"].numel() * 4 + h["grad"].numel() * 4 for h in host)
         bo = sum(st["n"] * 4 for st in state)
         h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        # Large gradients stream through in bucket-aligned chunks (H2D -> RS -> D2H per chunk), so
+        # the last group's result copy does not wait for its whole gradient: only the final chunk's
+        # D2H is left after the last H2D byte.  Same codes and results (comm.split_segments).
+        from paper_2302_02390_b200.comm import split_segments
+        e2e_chunk = 16 << 20  # bytes of gradient per chunk
+        for st in state:
+            nch = max(1, -(-st["g"].numel * 4 // e2e_chunk))
+            st["gparts"] = split_segments(st["segs"], args.bucket, nch)
 
         def step_e2e():
             main = torch.cuda.current_stream(dev)
@@ -557,10 +566,16 @@ def main():
                     e.record(h2d)
                     ev_shard.append(e)
                 for gi in range(len(state) - 1, -1, -1):
-                    state[gi]["grad"].copy_(host[gi]["grad"], non_blocking=True)
-                    e = torch.cuda.Event()
-                    e.record(h2d)
-                    ev_grad[gi] = e
+                    st, base = state[gi], state[gi]["segs"][0][0]
+                    ev_grad[gi] = []
+                    for sub in st["gparts"]:
+                        for s0, n0 in sub:
+                            if n0:
+                                st["grad"][s0 - base: s0 - base + n0].copy_(
+                                    host[gi]["grad"][s0 - base: s0 - base + n0], non_blocking=True)
+                        e = torch.cuda.Event()
+                        e.record(h2d)
+                        ev_grad[gi].append(e)
             for gi, st in enumerate(state):
                 main.wait_event(ev_shard[gi])
                 comm.all_gather(st["shard"], st["segs"], SegmentKey(0, 0, gi, 0, 0), st["full"])
@@ -571,19 +586,35 @@ def main():
                 e = torch.cuda.Event()
                 e.record(main)
                 rs_s.wait_event(e)
-                rs_s.wait_event(ev_grad[gi])
-                with torch.cuda.stream(rs_s):
-                    rs_comm.reduce_scatter(st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"])
-                    done = torch.cuda.Event()
-                    done.record(rs_s)
-                d2h.wait_event(done)
-                with torch.cuda.stream(d2h):
-                    h["res"][: st["n"]].copy_(st["gshard"][: st["n"]], non_blocking=True)
+                base, s_me = st["segs"][0][0], st["segs"][rank][0]
+                for sub, eg in zip(st["gparts"], ev_grad[gi]):
+                    rs_s.wait_event(eg)
+                    o0, on = sub[rank][0] - s_me, sub[rank][1]
+                    with torch.cuda.stream(rs_s):
+                        rs_comm.reduce_scatter(st["grad"][sub[0][0] - base:], sub, SegmentKey(0, 0, gi, 2, rank),
+                                               st["gshard"][o0:])
+                        done = torch.cuda.Event()
+                        done.record(rs_s)
+                    if on:
+                        d2h.wait_event(done)
+                        with torch.cuda.stream(d2h):
+                            h["res"][o0: o0 + on].copy_(st["gshard"][o0: o0 + on], non_blocking=True)
             for sidestream in (rs_stream, h2d, d2h):
                 main.wait_stream(sidestream)
             advance_counter(step_ctr)
 
         step_e2e()
+        torch.cuda.synchronize(dev)
+        if args.check_e2e:  # the chunked e2e results == one unchunked RS per group at the same step word
+            advance_counter(step_ctr, -1)
+            for gi, (st, h) in enumerate(zip(state, host)):
+                ref = torch.empty_like(st["gshard"])
+                rs_comm.reduce_scatter(st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), ref)
+                torch.cuda.synchronize(dev)
+                if not torch.equal(ref[: st["n"]].cpu(), h["res"][: st["n"]]):
+                    raise SystemExit(f"e2e check failed for group {gi}")
+            advance_counter(step_ctr, 1)
+            print(f"[rank {rank}] e2e chunked results match the unchunked reduce-scatter", file=sys.stderr)
         barrier()
         g_e2e = capture(step_e2e)
         g_e2e.replay()
@@ -599,7 +630,8 @@ def main():
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "ms_per_step": round(ems / args.steps, 3),
                "path": "QSDPComm -> qsdp_all_gather / qsdp_reduce_scatter (C ABI), pinned host buffers; "
                        "per-group H2D / D2H copies on two copy streams overlapping the collectives inside "
-                       "the step; one CUDA graph per step"}
+                       "the step (gradients > 16 MB in bucket-aligned chunks: H2D -> RS -> D2H); one CUDA "
+                       "graph per step"}
 
     # ---- GPT step/s: FSDP2 training step, unquantized (fp32 NCCL) vs QSDP comms ----
     gpt = None
