@@ -956,6 +956,8 @@ static bool push_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
 // S % 8 == 0, a whole warp per bucket (S >= 72), S * sizeof(T) <= 8 KB
 // (launch_q_t's routing), an fp32 / fp64 / bf16 output.
 static bool fdq_ok(const qsdp_qcfg* cfg, int in_dtype, int out_dtype) {
+  static const bool off = getenv("QSDP_NO_FDQ") != nullptr && getenv("QSDP_NO_FDQ")[0] == '1';  // A/B switch
+  if (off) return false;
   const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
   const int isz = in_dtype == QSDP_F64 ? 8 : 4;
   return cfg->inner != QSDP_INNER_LEVELS && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 72 &&
