@@ -413,7 +413,11 @@ def main():
                     "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
                     "bytes_per_launch": round(kernels[dom]["bytes_per_step"] / kernels[dom]["launches_per_step"]),
                     "method": "algorithmic bytes / CUDA-event time of that kernel's launches (graph of one step's "
-                              "launches of the kind, L2 flushed between replays)"}
+                              "launches of the kind, L2 flushed between replays)",
+                    "frac_by_kernel": {k: round(v["gbs"] / hbm_peak, 4) for k, v in kernels.items()}}
+        if dom.startswith("K2"):
+            roofline["note"] = ("K2 is integer-issue bound: one exact 128-bit PCG64 step per element "
+                                "(numpy's bucket_rng stream, DESIGN.md section 5)")
 
     # ---- learned-levels kernels on the same weight groups (world 1) ----
     levels = None
@@ -543,13 +547,14 @@ def main():
         bi = sum(h["shard"].numel() * 4 + h["grad"].numel() * 4 for h in host)
         bo = sum(st["n"] * 4 for st in state)
         h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-        # Large gradients stream through in bucket-aligned chunks (H2D -> RS -> D2H per chunk), so
-        # the last group's result copy does not wait for its whole gradient: only the final chunk's
-        # D2H is left after the last H2D byte.  Same codes and results (comm.split_segments).
+        # The last gradient of the backward order streams through in bucket-aligned chunks
+        # (H2D -> RS -> D2H per chunk), so its result copy does not wait for the whole gradient:
+        # only the final chunk's D2H is left after the last H2D byte.  Same codes and results
+        # (comm.split_segments).
         from paper_2302_02390_b200.comm import split_segments
         e2e_chunk = 16 << 20  # bytes of gradient per chunk
-        for st in state:
-            nch = max(1, -(-st["g"].numel * 4 // e2e_chunk))
+        for gi, st in enumerate(state):  # only the last gradient of the backward order is chunked
+            nch = max(1, -(-st["g"].numel * 4 // e2e_chunk)) if gi == 0 else 1
             st["gparts"] = split_segments(st["segs"], args.bucket, nch)
 
         def step_e2e():
@@ -630,12 +635,15 @@ def main():
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "ms_per_step": round(ems / args.steps, 3),
                "path": "QSDPComm -> qsdp_all_gather / qsdp_reduce_scatter (C ABI), pinned host buffers; "
                        "per-group H2D / D2H copies on two copy streams overlapping the collectives inside "
-                       "the step (gradients > 16 MB in bucket-aligned chunks: H2D -> RS -> D2H); one CUDA "
+                       "the step (the last gradient in 16 MB bucket-aligned chunks: H2D -> RS -> D2H); one CUDA "
                        "graph per step"}
 
     # ---- GPT step/s: FSDP2 training step, unquantized (fp32 NCCL) vs QSDP comms ----
     gpt = None
-    if not args.no_gpt:
+    if not args.no_gpt and world == 1:
+        gpt = {"skipped": "world 1: FSDP2 issues no collectives (QSDP and fp32 FSDP are the same step); "
+                          "measured at --gpus N > 1"}
+    elif not args.no_gpt:
         try:
             from paper_2302_02390_b200.gpt_train import build_model, run_training, shard_model
             gpt = {"model": args.model, "batch_per_gpu": args.gpt_batch, "seq": args.gpt_seq,
