@@ -993,7 +993,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
           }
           return m == 0u;
         };
-        if ((S & 127) == 0) {  // every lane owns exactly S/128 full groups
+        if ((S & 127) == 0 && f32ok) {  // every lane owns exactly S/128 full groups
           const int gfull = S >> 7;
 #pragma unroll 2
           for (int g = 0; g < gfull; ++g) {
@@ -1001,11 +1001,20 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             T v[4];
             lds_group(sb, 4 * gi, v);
             uint32_t c[4];
-            if (f32ok) {
-              if (code4f(v, c) && code4(v, c)) fix4(v, c);
-            } else if (code4(v, c)) {
-              fix4(v, c);
-            }
+            if (code4f(v, c) && code4(v, c)) fix4(v, c);  // rare: p ~ 2^-12 per element
+            const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
+            if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
+            if (fq4.out != nullptr) dq_emit4<BITS>(fq4, 4 * gi, 4, w);
+          }
+        } else if ((S & 127) == 0) {
+          const int gfull = S >> 7;
+#pragma unroll 2
+          for (int g = 0; g < gfull; ++g) {
+            const int gi = g * 32 + lane;
+            T v[4];
+            lds_group(sb, 4 * gi, v);
+            uint32_t c[4];
+            if (code4(v, c)) fix4(v, c);
             const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
             if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
             if (fq4.out != nullptr) dq_emit4<BITS>(fq4, 4 * gi, 4, w);
