@@ -36,6 +36,25 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
 
+def pin_to_gpu_numa(local: int) -> None:
+    """Run this rank on the CPUs next to its GPU (the PCIe root's NUMA node), so the pinned host
+    buffers of the e2e step are allocated in local memory.  No-op where sysfs does not say."""
+    import torch
+    try:
+        p = torch.cuda.get_device_properties(local)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        spec = open(f"/sys/bus/pci/devices/{bus}/local_cpulist").read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+    except Exception:
+        pass
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -211,6 +230,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    pin_to_gpu_numa(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     _lib.lib()
@@ -326,7 +346,7 @@ def main():
     launches = comm_launches()
     klaunches = local_launches() if world == 1 else []
     per_coll = 1 if comm_fused else (3 if world > 1 else 2)
-    n_launch = len(launches) * per_coll + 1  # + step counter
+    n_launch = len(launches) * per_coll + 1  # + step counter (replaced by the captured graph's kernel-node count)
 
     def run_step(sel=None):
         if sel is None:
@@ -342,11 +362,29 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    def capture(fn):
-        g = torch.cuda.CUDAGraph()
+    def capture(fn, keep=False):
+        try:
+            g = torch.cuda.CUDAGraph(keep_graph=keep)
+        except TypeError:
+            g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             fn()
         return g
+
+    def kernel_nodes(g):
+        """Kernel nodes of a captured step graph (every one is a launch of this library's kernels:
+        the step holds only the communicator's collectives and the step-counter update)."""
+        try:
+            from cuda.bindings import runtime as rt
+            h = rt.cudaGraph_t(init_value=g.raw_cuda_graph())
+            err, _, n = rt.cudaGraphGetNodes(h, 0)
+            err, nodes, n = rt.cudaGraphGetNodes(h, n)
+            if err != rt.cudaError_t.cudaSuccess:
+                return None
+            return sum(1 for nd in nodes
+                       if rt.cudaGraphNodeGetType(nd)[1] == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel)
+        except Exception:
+            return None
 
     def time_graph(g, reps, flush_between=True):
         ev = []
@@ -363,7 +401,10 @@ def main():
     for _ in range(args.warmup):
         run_step()
     barrier()
-    g_step = capture(run_step)
+    g_step = capture(run_step, keep=True)
+    nodes = kernel_nodes(g_step)
+    if nodes is not None:
+        n_launch = nodes
     for _ in range(args.warmup):  # warm the graph itself
         g_step.replay()
     barrier()
@@ -401,6 +442,35 @@ def main():
             kernels[k] = {"ms_per_step": round(tk, 4), "launches_per_step": cnt, "avg_launch_us": round(tk / cnt * 1e3, 2),
                           "gbs": round(nb / (tk * 1e-3) / 1e9, 1), "share_of_step": round(tk / ms_step, 4),
                           "bytes_per_step": nb}
+        # The step's own launches: at world 1 each collective is ONE quantizer launch with the fused
+        # dequant epilogue (AG: K1 + K3 of the own shard; RS: K2 + K4's 0.0 + v), so the roofline is
+        # taken over those kinds, timed the same way; the four standalone kernels (the N > 1 path and
+        # the batch API) stay listed as kernels_unfused.
+        osz = 4 if out_dt == torch.float32 else 2
+        fused_kinds = {}
+        for kind, sel in (("AG_K1_fused_dequant", "AG"), ("RS_K2_fused_dequant", "RS")):
+            fns = [x[2] for x in launches if x[0] == sel]
+            gk = capture(lambda fns=fns: [f() for f in fns], keep=True)
+            cnt = kernel_nodes(gk) or len(fns)
+            if cnt != len(fns):  # not fused for this config: keep the standalone breakdown
+                fused_kinds = {}
+                break
+            gk.replay()
+            torch.cuda.synchronize(dev)
+            evk = time_graph(gk, args.steps)
+            torch.cuda.synchronize(dev)
+            tk = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+            reps = 2 if sel == "AG" else 1
+            nb = reps * sum(4 * st["n"] + (osz if sel == "AG" else 4) * st["n"] + 12 * num_buckets(st["n"], args.bucket)
+                            for st in state)
+            fused_kinds[kind] = {"ms_per_step": round(tk, 4), "launches_per_step": cnt,
+                                 "avg_launch_us": round(tk / cnt * 1e3, 2), "gbs": round(nb / (tk * 1e-3) / 1e9, 1),
+                                 "share_of_step": round(tk / ms_step, 4), "bytes_per_step": nb,
+                                 "bytes_per_element": f"4 in + {osz if sel == 'AG' else 4} out + 12/{args.bucket} meta "
+                                                      "(no codes: world 1 has no reader)"}
+        kernels_unfused = None
+        if fused_kinds:
+            kernels_unfused, kernels = kernels, fused_kinds
         dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
         ach = kernels[dom]["gbs"]
         traffic = None
@@ -415,9 +485,11 @@ def main():
                     "method": "algorithmic bytes / CUDA-event time of that kernel's launches (graph of one step's "
                               "launches of the kind, L2 flushed between replays)",
                     "frac_by_kernel": {k: round(v["gbs"] / hbm_peak, 4) for k, v in kernels.items()}}
-        if dom.startswith("K2"):
+        if "K2" in dom:
             roofline["note"] = ("K2 is integer-issue bound: one exact 128-bit PCG64 step per element "
                                 "(numpy's bucket_rng stream, DESIGN.md section 5)")
+        if kernels_unfused is not None:
+            roofline["frac_by_kernel_unfused"] = {k: round(v["gbs"] / hbm_peak, 4) for k, v in kernels_unfused.items()}
 
     # ---- learned-levels kernels on the same weight groups (world 1) ----
     levels = None
@@ -683,7 +755,7 @@ def main():
                        "parallelism": f"qsdp{world}", "execution": "one CUDA graph per step (device step counter), "
                                     + ("fused single-launch collectives" if comm_fused else "3 launches per collective"),
                        "convention": "sum over ranks of 4*N per collective / time"},
-            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
+            "roofline": roofline, "kernels": kernels, "kernels_unfused": kernels_unfused if world == 1 else None, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
             "levels": levels, "wire": wire, "lattice": lattice,
             "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),
         }
