@@ -638,20 +638,21 @@ struct FusedDq {
   double lo, pitch, shift;
   int dtype, add0;
 };
-template <int BITS>
+// FDQ variants: 0 none; 1 fp32 out; 2 fp32 out with K4's 0.0 + v; 3 dtype / add0 read at run time.
+template <int BITS, int FDQ>
 __device__ __forceinline__ void dq_emit4(const FusedDq& f, int e, int n_left, uint64_t w) {
   double v[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const double c = code_to_double((uint32_t)((w >> (i * BITS)) & ((1ull << BITS) - 1ull)));
     v[i] = __dadd_rn(__dadd_rn(f.lo, __dmul_rn(c, f.pitch)), f.shift);
-    if (f.add0) v[i] = __dadd_rn(0.0, v[i]);
+    if (FDQ == 2 || (FDQ == 3 && f.add0)) v[i] = __dadd_rn(0.0, v[i]);
   }
-  if (f.dtype == 0) store_out4<0, true>(f.out, e, n_left, v);
+  if (FDQ == 1 || FDQ == 2 || f.dtype == 0) store_out4<0, true>(f.out, e, n_left, v);
   else if (f.dtype == 1) store_out4<1, true>(f.out, e, n_left, v);
   else store_out4<2, true>(f.out, e, n_left, v);
 }
-template <bool FDQ>
+template <int FDQ>
 __device__ __forceinline__ FusedDq fused_dq(const QJobTable& tab, const QJob& J, int64_t off, float lof, float hif,
                                             float shift_f, int bits) {
   FusedDq f;
@@ -671,7 +672,7 @@ __device__ __forceinline__ FusedDq fused_dq(const QJobTable& tab, const QJob& J,
 // Partial / unaligned / degenerate bucket (one per segment at most on the hot
 // path): per-lane seeding and the Coder path; out of line to keep the fast
 // loop's register budget.  Returns the bucket's f32 shift.
-template <typename T, int INNER, int BITS, bool FDQ = false>
+template <typename T, int INNER, int BITS, int FDQ = 0>
 static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix& seed, uint64_t start, const T* x, int n,
                                                              int gl, uint8_t* cbase, float lof, float hif,
                                                              bool degenerate, int lane, const QJobTable& tab,
@@ -692,7 +693,7 @@ static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix
         w = cd.group(v, e, n, BITS);
       }
       if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, pb, e + 4 <= n);
-      if (fq.out != nullptr) dq_emit4<BITS>(fq, e, n - e, w);
+      if (fq.out != nullptr) dq_emit4<BITS, FDQ>(fq, e, n - e, w);
     }
   }
   return shift_f;
@@ -802,7 +803,7 @@ struct JobCursor {
   }
 };
 
-template <typename T, int INNER, int BITS, int NST, bool FDQ = false>
+template <typename T, int INNER, int BITS, int NST, int FDQ = 0>
 __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_t* smem) {
   const int64_t poff = q_parity_off(tab);
   using Tr = InTraits<T>;
@@ -1004,7 +1005,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             if (code4f(v, c) && code4(v, c)) fix4(v, c);  // rare: p ~ 2^-12 per element
             const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
             if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
-            if (fq4.out != nullptr) dq_emit4<BITS>(fq4, 4 * gi, 4, w);
+            if (fq4.out != nullptr) dq_emit4<BITS, FDQ>(fq4, 4 * gi, 4, w);
           }
         } else if ((S & 127) == 0) {
           const int gfull = S >> 7;
@@ -1017,7 +1018,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             if (code4(v, c)) fix4(v, c);
             const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
             if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
-            if (fq4.out != nullptr) dq_emit4<BITS>(fq4, 4 * gi, 4, w);
+            if (fq4.out != nullptr) dq_emit4<BITS, FDQ>(fq4, 4 * gi, 4, w);
           }
         } else {
           for (int g = 0; g < gl; ++g) {
@@ -1030,7 +1031,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
               if (code4(v, c)) fix4(v, c);
               const uint64_t w = pack4<BITS>(c[0], c[1], c[2], c[3]);
               if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
-              if (fq4.out != nullptr) dq_emit4<BITS>(fq4, e, n - e, w);
+              if (fq4.out != nullptr) dq_emit4<BITS, FDQ>(fq4, e, n - e, w);
             }
           }
         }
@@ -1069,8 +1070,8 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
           if (unc) w = stoch_octet_exact<T, BITS>(sb + 8 * o, st0, inc, lo, span, K1, top);
           if (!FDQ || !tab.dq_nocodes) store_octet<BITS>(cbase, o, w);
           if (fqs.out != nullptr) {
-            dq_emit4<BITS>(fqs, 8 * o, 4, w);
-            dq_emit4<BITS>(fqs, 8 * o + 4, 4, w >> (4 * BITS));
+            dq_emit4<BITS, FDQ>(fqs, 8 * o, 4, w);
+            dq_emit4<BITS, FDQ>(fqs, 8 * o + 4, 4, w >> (4 * BITS));
           }
           st = add128(mul128(OJa, st), jc);
         }
@@ -1106,7 +1107,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             }
             st = add128(mul128(JA, st), jc);
             if (!FDQ || !tab.dq_nocodes) store_direct<BITS>(cbase, gi, w, 0, true);
-            if (fqq.out != nullptr) dq_emit4<BITS>(fqq, e, n - e, w);
+            if (fqq.out != nullptr) dq_emit4<BITS, FDQ>(fqq, e, n - e, w);
           }
         }
       }
@@ -1127,7 +1128,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
   }
 }
 
-template <typename T, int INNER, int BITS, int NST, bool FDQ = false>
+template <typename T, int INNER, int BITS, int NST, int FDQ = 0>
 __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_constant__ QJobTable tab) {
   extern __shared__ __align__(128) uint8_t smem[];
   quantize_tma32_body<T, INNER, BITS, NST, FDQ>(tab, smem);
@@ -1953,7 +1954,7 @@ __global__ void __launch_bounds__(256, 2) fused_collective_kernel(const __grid_c
                                                                   const __grid_constant__ FuseSync fs) {
   extern __shared__ __align__(128) uint8_t smem[];
   const unsigned long long target = ld_dev_u64(fs.epoch) + 1ull;
-  quantize_tma32_body<T, INNER, BITS, NST, true>(qt, smem);
+  quantize_tma32_body<T, INNER, BITS, NST, 3>(qt, smem);
   fused_barrier(fs, target);
   // the phase-A ring is free again: reuse its start for the per-source scale rows
   dequant_body<BITS, 32, OUT, true, ACC, true>(dt, reinterpret_cast<double*>(smem));
@@ -1995,7 +1996,7 @@ inline int persistent_grid(F kern, int threads, size_t smem, int64_t total_bucke
 }
 
 // Fast TMA path.  Returns false when the configuration needs the general kernel.
-template <typename T, int INNER, int BITS, bool FDQ>
+template <typename T, int INNER, int BITS, int FDQ>
 cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
   constexpr int NST = 2;
   const size_t stage = (size_t)tab.bucket * sizeof(T);
@@ -2020,7 +2021,10 @@ template <typename T, int INNER, int BITS>
 cudaError_t launch_q_tma32(const QJobTable& tab, int sms, cudaStream_t s) {
   bool fdq = false;
   for (int j = 0; j < tab.njobs; ++j) fdq = fdq || tab.jobs[j].dq_out != nullptr;
-  return fdq ? launch_q_tma32_v<T, INNER, BITS, true>(tab, sms, s) : launch_q_tma32_v<T, INNER, BITS, false>(tab, sms, s);
+  if (!fdq) return launch_q_tma32_v<T, INNER, BITS, 0>(tab, sms, s);
+  if (sizeof(T) == 4 && tab.dq_dtype == 0)  // fp32 out: dtype and K4's 0.0 + v fixed at compile time
+    return tab.dq_add0 ? launch_q_tma32_v<T, INNER, BITS, 2>(tab, sms, s) : launch_q_tma32_v<T, INNER, BITS, 1>(tab, sms, s);
+  return launch_q_tma32_v<T, INNER, BITS, 3>(tab, sms, s);
 }
 
 template <typename T, int INNER, int BITS, int TL>
