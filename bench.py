@@ -268,15 +268,9 @@ def main():
     comm.set_step_source(step_ctr)
     # FSDP2's schedule (fsdp.QSDPContext): reduce-scatters on their own stream with their own
     # communicator, RS(i) after AG(i)'s backward re-gather, overlapping AG(i-1)
-    if os.environ.get("QSDP_FUSED", "0") == "1":
-        # a fused collective holds a grid-wide barrier: it needs every CTA resident, so it
-        # must never share the GPU with another collective stream
-        args.serial = True
     rs_comm = comm if args.serial else QSDPComm(max_seg, wspec, gspec, device=dev)
     rs_comm.set_step_source(step_ctr)
     rs_stream = torch.cuda.Stream(device=dev)
-    comm_fused = os.environ.get("QSDP_FUSED", "0") == "1" and args.bucket % 8 == 0 and 128 <= args.bucket <= 2048 \
-        and args.wbits in (2, 4, 8, 16) and args.gbits in (2, 4, 8, 16)
     stream = torch.cuda.current_stream(dev)
 
     # ---- the step as a list of launches (kind, bytes, fn) ----
@@ -341,11 +335,11 @@ def main():
         if forked:
             main.wait_stream(rs_stream)
 
-    # `value` times the product path (the communicator: one fused launch per collective when
-    # possible); the per-kernel roofline graphs replay the same kernels through the batch API.
+    # `value` times the product path (the communicator); the per-kernel roofline graphs replay
+    # the same kernels through the batch API.
     launches = comm_launches()
     klaunches = local_launches() if world == 1 else []
-    per_coll = 1 if comm_fused else (3 if world > 1 else 2)
+    per_coll = 3 if world > 1 else 1  # world 1: one quantizer launch with the fused dequant
     n_launch = len(launches) * per_coll + 1  # + step counter (replaced by the captured graph's kernel-node count)
 
     def run_step(sel=None):
@@ -753,7 +747,8 @@ def main():
                        "out_dtype": args.out_dtype, "quantizer_input": "f32", "arithmetic": "f64 (bit-exact)",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 126 MB L2",
                        "parallelism": f"qsdp{world}", "execution": "one CUDA graph per step (device step counter), "
-                                    + ("fused single-launch collectives" if comm_fused else "3 launches per collective"),
+                                    + ("quantize + barrier + dequantize launches per collective" if world > 1
+                                       else "one quantizer launch (fused dequant) per collective"),
                        "convention": "sum over ranks of 4*N per collective / time"},
             "roofline": roofline, "kernels": kernels, "kernels_unfused": kernels_unfused if world == 1 else None, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
             "levels": levels, "wire": wire, "lattice": lattice,

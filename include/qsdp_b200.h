@@ -45,7 +45,7 @@
  *   QSDP_EDECODE / QSDP_ETRUNC / QSDP_EVERSION   DecodeError / TruncatedMessageError /
  *                   UnsupportedVersionError (qsdp_wire_parse / qsdp_wire_decode_device)
  *   QSDP_ECUDA      CUDA runtime failure (message in qsdp_last_error())
- *   QSDP_EPEER      peer-memory / IPC setup failure
+ *   QSDP_EPEER      peer-memory / IPC setup failure, or a peer missed a barrier (timeout)
  */
 #ifndef QSDP_B200_H_
 #define QSDP_B200_H_
@@ -245,16 +245,20 @@ qsdp_status qsdp_comm_open_peers(qsdp_comm* c, const void* handles /* world*QSDP
  * With it, and the communicator's device-side epoch, a sequence of
  * qsdp_all_gather / qsdp_reduce_scatter calls can be captured in a CUDA graph. */
 qsdp_status qsdp_comm_set_step_source(qsdp_comm* c, const uint64_t* d_step);
-/* 1 (opt-in; env QSDP_FUSED=1 sets it at creation): run each collective as ONE persistent
- * kernel -- quantize, in-kernel grid + cross-GPU barrier, pull-dequantize -- when the
- * configuration allows (fp32 input, 2/4/8/16 bits, bucket 128..2048, aligned output). */
 /* Learned weight levels for the all-gather (w.inner == QSDP_INNER_LEVELS): a
  * device float64[2^w.bits] table that stays valid while the comm uses it. */
 qsdp_status qsdp_comm_set_weight_levels(qsdp_comm* c, const double* d_levels, int32_t nlevels);
 /* Size the collectives' grids for at most `sms` SMs (0 = all): leaves the rest of the
  * GPU to compute kernels that run concurrently (FSDP2 overlaps comm streams with compute). */
 qsdp_status qsdp_comm_set_sm_budget(qsdp_comm* c, int32_t sms);
-qsdp_status qsdp_comm_set_fused(qsdp_comm* c, int32_t enable);
+/* Failure detection.  A barrier whose peer does not arrive within the timeout
+ * (default 60 s; env QSDP_TIMEOUT_MS at creation) gives up instead of hanging and
+ * records the peer in a host-mapped word: qsdp_comm_status() -- and every later
+ * qsdp_all_gather / qsdp_reduce_scatter -- then returns QSDP_EPEER naming the peer
+ * and epoch (the data of that collective is undefined).  qsdp_comm_status() does
+ * not synchronise: call it after the stream has completed the collectives to check. */
+qsdp_status qsdp_comm_set_timeout(qsdp_comm* c, int64_t timeout_ms);
+qsdp_status qsdp_comm_status(qsdp_comm* c);
 /* Quantized all-gather (ShardedMLP._gather): this rank's shard = segs[rank];
  * every rank writes the dequantized full tensor (sum of segs lengths) to full_out.
  * key->worker is forced to 0 (sharded.py:341). */

@@ -38,12 +38,12 @@ EXPORTED_SYMBOLS = (
     "qsdp_dequantize_batch", "qsdp_dequant_accumulate", "qsdp_dequant_accumulate_batch",
     "qsdp_wire_encode", "qsdp_comm_create", "qsdp_comm_ipc_handle", "qsdp_comm_open_peers",
     "qsdp_all_gather", "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_batch_dstep",
-    "qsdp_counter_add", "qsdp_comm_set_step_source", "qsdp_comm_set_fused",
+    "qsdp_counter_add", "qsdp_comm_set_step_source",
     "qsdp_quantize_levels", "qsdp_quantize_levels_batch", "qsdp_dequantize_levels",
     "qsdp_dequantize_levels_batch", "qsdp_learn_levels", "qsdp_comm_set_weight_levels",
     "qsdp_wire_parse", "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes",
     "qsdp_unpack_codes", "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice",
-    "qsdp_comm_set_sm_budget",
+    "qsdp_comm_set_sm_budget", "qsdp_comm_set_timeout", "qsdp_comm_status",
 )
 
 
@@ -149,9 +149,10 @@ def lib():
     L.qsdp_quantize_batch_dstep.argtypes = [ctypes.POINTER(QItem), i32, i32, cfgp, vp, vp, vp]
     L.qsdp_counter_add.argtypes = [vp, ctypes.c_uint64, vp]
     L.qsdp_comm_set_step_source.argtypes = [vp, vp]
-    L.qsdp_comm_set_fused.argtypes = [vp, i32]
     L.qsdp_comm_set_weight_levels.argtypes = [vp, vp, i32]
     L.qsdp_comm_set_sm_budget.argtypes = [vp, i32]
+    L.qsdp_comm_set_timeout.argtypes = [vp, i64]
+    L.qsdp_comm_status.argtypes = [vp]
     L.qsdp_wire_parse.argtypes = [vp, i64, ctypes.POINTER(WireInfo)]
     L.qsdp_wire_encode_device.argtypes = [vp, vp, i64, cfgp, vp, i64, vp]
     L.qsdp_wire_decode_device.argtypes = [vp, ctypes.POINTER(WireInfo), vp, vp, vp, vp]
@@ -179,14 +180,15 @@ def lib():
     L.qsdp_dequantize_levels_batch.argtypes = [ctypes.POINTER(DItem), i32, cfgp, vp, i32, i32, vp]
     L.qsdp_learn_levels.argtypes = [vp, i64, vp, i32, ctypes.c_double, vp]
     for name in ("qsdp_quantize", "qsdp_quantize_batch", "qsdp_quantize_batch_dstep", "qsdp_counter_add",
-                 "qsdp_comm_set_step_source", "qsdp_comm_set_fused", "qsdp_dequantize", "qsdp_dequantize_batch",
+                 "qsdp_comm_set_step_source", "qsdp_dequantize", "qsdp_dequantize_batch",
                  "qsdp_dequant_accumulate", "qsdp_dequant_accumulate_batch", "qsdp_comm_create",
                  "qsdp_comm_ipc_handle", "qsdp_comm_open_peers", "qsdp_all_gather",
                  "qsdp_reduce_scatter", "qsdp_comm_destroy", "qsdp_quantize_levels",
                  "qsdp_quantize_levels_batch", "qsdp_dequantize_levels", "qsdp_dequantize_levels_batch",
                  "qsdp_learn_levels", "qsdp_comm_set_weight_levels", "qsdp_wire_parse",
                  "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes", "qsdp_unpack_codes",
-                 "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice", "qsdp_comm_set_sm_budget"):
+                 "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice", "qsdp_comm_set_sm_budget",
+                 "qsdp_comm_set_timeout", "qsdp_comm_status"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib

@@ -173,11 +173,16 @@ class QSDPComm:
         collectives overlapping compute on another stream leave it the other SMs."""
         _lib.check(_lib.lib().qsdp_comm_set_sm_budget(self._h, int(sms)))
 
-    def set_fused(self, enable: bool) -> None:
-        """Single-launch fused collectives (opt-in; env QSDP_FUSED=1 sets the default).
-        A fused collective holds a grid-wide barrier and needs every CTA resident:
-        use it only when no other collective runs concurrently on this GPU (one stream)."""
-        _lib.check(_lib.lib().qsdp_comm_set_fused(self._h, 1 if enable else 0))
+    def set_timeout(self, ms: int) -> None:
+        """Barrier timeout: a peer that does not arrive within ``ms`` milliseconds makes the
+        barrier give up instead of hanging; :meth:`check` (and every later collective)
+        then raises :class:`~._lib.QSDPError` naming the peer."""
+        _lib.check(_lib.lib().qsdp_comm_set_timeout(self._h, int(ms)))
+
+    def check(self) -> None:
+        """Raise if a peer missed a barrier of an already-completed collective (does not
+        synchronise: call it after the stream has run the collectives)."""
+        _lib.check(_lib.lib().qsdp_comm_status(self._h))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -34,8 +34,6 @@ cudaError_t launch_quantize_f64(const QJobTable& tab, bool vec, int sms, cudaStr
 cudaError_t launch_dequant(const DJobTable& tab, bool vec, int sms, cudaStream_t s);
 cudaError_t upload_jump_f32(const JumpEntry* host);
 cudaError_t upload_jump_f64(const JumpEntry* host);
-cudaError_t upload_jump_fused(const JumpEntry* host);
-cudaError_t launch_fused(const QJobTable& qt, const DJobTable& dt, const FuseSync& fs, int sms, cudaStream_t s);
 cudaError_t launch_quantize_levels(const QJobTable& tab, int in_f64, const double* levels, int nl, bool vec, int sms,
                                    cudaStream_t s);
 cudaError_t launch_dequant_levels(const DJobTable& tab, const double* levels, bool vec, int sms, cudaStream_t s);
@@ -96,7 +94,6 @@ qsdp_status ensure_device(int& sms) {
     }
     QSDP_CUDA(upload_jump_f32(tab));
     QSDP_CUDA(upload_jump_f64(tab));
-    QSDP_CUDA(upload_jump_fused(tab));
     QSDP_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
     d.jump_ready = true;
   }
@@ -147,7 +144,7 @@ struct DynSrc {
   int64_t mirror_delta[QSDP_FUSE_MAX_WORLD - 1] = {};
 };
 
-// Table builders shared by the launch-per-stage path and the fused collectives.
+// Table builders of the quantize / dequantize launches.
 void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, const qsdp_qcfg* cfg, uint64_t* d_bad,
                 const DynSrc& dyn, bool& vec) {
   memset(&tab, 0, sizeof(tab));
@@ -717,7 +714,20 @@ struct PeerFlags {
 
 constexpr size_t kEpochOff = 128;
 
-__global__ void qsdp_barrier_kernel(PeerFlags pf, int rank, int world, unsigned long long* epoch_ptr) {
+// Failure detection: a peer that never arrives (dead, hung or desynchronised)
+// must not hang this rank.  Each waiting lane gives up after `timeout_ns` of
+// %globaltimer and records (peer + 1) | (target epoch << 8) in a host-mapped
+// word; the host surfaces it as QSDP_EPEER at the next collective or
+// qsdp_comm_status() call (errors propagate, never hang -- quantize.py:41-44's
+// contract carried over to the transport).
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void qsdp_barrier_kernel(PeerFlags pf, int rank, int world, unsigned long long* epoch_ptr,
+                                    unsigned long long* err_word, unsigned long long timeout_ns) {
   const int t = threadIdx.x;
   const unsigned long long target = *reinterpret_cast<volatile unsigned long long*>(epoch_ptr) + 1ull;
   if (t < world) {
@@ -725,10 +735,17 @@ __global__ void qsdp_barrier_kernel(PeerFlags pf, int rank, int world, unsigned 
     unsigned long long* dst = pf.flags[t] + rank;  // peer t learns "rank reached target"
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(target) : "memory");
     const unsigned long long* mine = pf.flags[rank] + t;
+    const unsigned long long t0 = globaltimer_ns();
     unsigned long long v = 0;
-    do {
+    for (unsigned it = 0;; ++it) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
-    } while (v < target);
+      if (v >= target) break;
+      if ((it & 255u) == 255u && globaltimer_ns() - t0 > timeout_ns) {
+        atomicCAS(err_word, 0ull, (unsigned long long)(t + 1) | (target << 8));
+        __threadfence_system();
+        break;
+      }
+    }
   }
   __syncthreads();
   if (t == 0) *reinterpret_cast<volatile unsigned long long*>(epoch_ptr) = target;
@@ -746,10 +763,12 @@ struct qsdp_comm {
   uint8_t* peer[QSDP_MAX_WORLD] = {};
   bool opened[QSDP_MAX_WORLD] = {};
   const unsigned long long* step_src = nullptr;
-  bool fused = true;  // single-launch collectives when the configuration allows
   int sm_budget = 0;                // > 0: the collectives' kernels use at most this many SMs
   const double* wlevels = nullptr;  // learned weight table (w.inner == QSDP_INNER_LEVELS)
   int wnlevels = 0;
+  unsigned long long* err_host = nullptr;  // host-mapped failure word (barrier timeout)
+  unsigned long long* err_dev = nullptr;
+  unsigned long long timeout_ns = 0;
 
   static constexpr size_t kFlagBytes = 256;
   uint8_t* slot(uint8_t* b, int idx) const { return b + kFlagBytes + (size_t)idx * slot_bytes; }  // parity 0
@@ -809,10 +828,18 @@ qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32
     return cuda_fail(e, "cudaMemset(comm workspace)");
   }
   c->peer[rank] = c->base;
-  // fused single-launch collectives are opt-in until their pull phase is TMA-staged
-  // (measured slower than the 3-launch path in round 1)
-  const char* env = getenv("QSDP_FUSED");
-  c->fused = env != nullptr && env[0] == '1';
+  e = cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(unsigned long long), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0);
+  if (e != cudaSuccess) {
+    if (c->err_host) cudaFreeHost(c->err_host);
+    cudaFree(c->base);
+    delete c;
+    return cuda_fail(e, "cudaHostAlloc(comm failure word)");
+  }
+  *reinterpret_cast<volatile unsigned long long*>(c->err_host) = 0;
+  // default barrier timeout 60 s (QSDP_TIMEOUT_MS overrides; qsdp_comm_set_timeout at run time)
+  const char* tmo = getenv("QSDP_TIMEOUT_MS");
+  c->timeout_ns = (unsigned long long)(tmo != nullptr ? atoll(tmo) : 60000ll) * 1000000ull;
   *out = c;
   return QSDP_OK;
 }
@@ -833,10 +860,17 @@ qsdp_status qsdp_comm_set_sm_budget(qsdp_comm* c, int32_t sms) {
   return QSDP_OK;
 }
 
-qsdp_status qsdp_comm_set_fused(qsdp_comm* c, int32_t enable) {
-  if (c == nullptr) return fail(QSDP_EINVAL, "null comm");
-  c->fused = enable != 0;
+static qsdp_status comm_failed(const qsdp_comm* c);
+
+qsdp_status qsdp_comm_set_timeout(qsdp_comm* c, int64_t timeout_ms) {
+  if (c == nullptr || timeout_ms < 1) return fail(QSDP_EINVAL, "timeout must be >= 1 ms");
+  c->timeout_ns = (unsigned long long)timeout_ms * 1000000ull;
   return QSDP_OK;
+}
+
+qsdp_status qsdp_comm_status(qsdp_comm* c) {
+  if (c == nullptr) return fail(QSDP_EINVAL, "null comm");
+  return comm_failed(c);
 }
 
 qsdp_status qsdp_comm_set_step_source(qsdp_comm* c, const uint64_t* d_step) {
@@ -878,8 +912,19 @@ qsdp_status qsdp_comm_destroy(qsdp_comm* c) {
   for (int j = 0; j < c->world; ++j)
     if (c->opened[j]) cudaIpcCloseMemHandle(c->peer[j]);
   if (c->base) cudaFree(c->base);
+  if (c->err_host) cudaFreeHost(c->err_host);
   delete c;
   return QSDP_OK;
+}
+
+// A peer failed to arrive at an earlier barrier: every later collective fails fast.
+static qsdp_status comm_failed(const qsdp_comm* c) {
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(c->err_host);
+  if (e == 0) return QSDP_OK;
+  const int peer = (int)(e & 255ull) - 1;
+  return fail(QSDP_EPEER, "rank " + std::to_string(c->rank) + ": peer " + std::to_string(peer) +
+                              " did not arrive at barrier epoch " + std::to_string(e >> 8) + " within " +
+                              std::to_string(c->timeout_ns / 1000000ull) + " ms");
 }
 
 static qsdp_status comm_barrier(qsdp_comm* c, cudaStream_t s) {
@@ -889,7 +934,7 @@ static qsdp_status comm_barrier(qsdp_comm* c, cudaStream_t s) {
     if (c->peer[j] == nullptr) return fail(QSDP_EPEER, "peers not opened");
     pf.flags[j] = reinterpret_cast<unsigned long long*>(c->peer[j]);
   }
-  qsdp_barrier_kernel<<<1, 32, 0, s>>>(pf, c->rank, c->world, c->epoch());
+  qsdp_barrier_kernel<<<1, 32, 0, s>>>(pf, c->rank, c->world, c->epoch(), c->err_dev, c->timeout_ns);
   QSDP_CUDA(cudaGetLastError());
   return QSDP_OK;
 }
@@ -935,14 +980,6 @@ static QJobSpec comm_qjob(const void* x, const qsdp_segment& seg, uint8_t* slot,
   return q;
 }
 
-// The fused single-launch collective covers the hot configuration: fp32 input,
-// direct widths, buckets of 128..2048 elements, vector-aligned outputs.
-static bool fused_cfg_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
-  const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
-  return c->fused && cfg->inner != QSDP_INNER_LEVELS && in_dtype == QSDP_F32 && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 128 &&
-         cfg->bucket * 4 <= 8192;
-}
-
 // The push all-gather needs the quantizer that copies buckets out (the TMA32
 // kernel: direct widths, S % 8 == 0, 72 <= S, S * sizeof(T) <= 8 KB).
 static bool push_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
@@ -964,46 +1001,12 @@ static bool fdq_ok(const qsdp_qcfg* cfg, int in_dtype, int out_dtype) {
          cfg->bucket * isz <= 8192 && (out_dtype == QSDP_F32 || out_dtype == QSDP_F64 || out_dtype == QSDP_BF16);
 }
 
-static FuseSync comm_sync(const qsdp_comm* c) {
-  FuseSync fs;
-  memset(&fs, 0, sizeof(fs));
-  fs.epoch = c->epoch();
-  fs.arrive = reinterpret_cast<unsigned int*>(c->base + kEpochOff + 8);
-  fs.go = reinterpret_cast<unsigned long long*>(c->base + kEpochOff + 16);
-  for (int j = 0; j < c->world; ++j) fs.flags[j] = reinterpret_cast<unsigned long long*>(c->peer[j]);
-  fs.rank = c->rank;
-  fs.world = c->world;
-  return fs;
-}
-
-// Returns QSDP_OK if launched, QSDP_EINVAL (silently) if the fused path does not apply.
-static qsdp_status try_fused(qsdp_comm* c, const std::vector<QJobSpec>& q, const std::vector<DJobSpec>& d,
-                             const qsdp_qcfg* cfg, int accumulate, int divisor, int out_dtype, cudaStream_t s,
-                             const DynSrc& qdyn, bool& launched) {
-  launched = false;
-  for (int j = 0; j < c->world; ++j)
-    if (c->peer[j] == nullptr) return fail(QSDP_EPEER, "peers not opened");
-  QJobTable qt;
-  DJobTable dt;
-  size_t qi = 0, di = 0;
-  bool qvec = false, dvec = false;
-  build_qtab(qt, q, qi, cfg, nullptr, qdyn, qvec);
-  build_dtab(dt, d, di, cfg, accumulate, divisor, out_dtype, comm_dyn(c, 0), dvec);
-  if (qi != q.size() || di != d.size() || !dvec || !dt.codes_vec) return QSDP_OK;
-  if (out_dtype != QSDP_F32 && !(out_dtype == QSDP_BF16 && !accumulate)) return QSDP_OK;
-  int sms = 0;
-  qsdp_status st = ensure_device(sms);
-  if (st != QSDP_OK) return st;
-  cudaError_t e = launch_fused(qt, dt, comm_sync(c), sms, s);
-  if (e != cudaSuccess) return cuda_fail(e, "fused collective launch");
-  launched = true;
-  return QSDP_OK;
-}
-
 qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, const qsdp_segment* segs,
                             const qsdp_key* key, void* full_out, int32_t out_dtype, void* stream) {
   if (c == nullptr || key == nullptr) return fail(QSDP_EINVAL, "null argument");
-  qsdp_status st = check_segs(c, segs);
+  qsdp_status st = comm_failed(c);
+  if (st != QSDP_OK) return st;
+  st = check_segs(c, segs);
   if (st != QSDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const qsdp_qcfg* cfg = &c->w;
@@ -1025,9 +1028,12 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
   const size_t osz = dtype_size(out_dtype);
   // this rank's own shard is dequantized by the quantizer itself (fused epilogue):
   // the dequant launch covers the peers' shards only (none at world 1)
-  const bool fdq = fdq_ok(cfg, in_dtype, out_dtype);
+  // (vector stores: the shard's first output element must be 16-byte aligned, 8 for bf16 --
+  // shard_bounds offsets need not be multiples of 4; otherwise K3 covers the own shard too)
+  uint8_t* own_out = static_cast<uint8_t*>(full_out) + (size_t)(segs[c->rank].global_start - segs[0].global_start) * osz;
+  const bool fdq = fdq_ok(cfg, in_dtype, out_dtype) && aligned(own_out, osz == 2 ? 8 : 16);
   if (fdq) {
-    q[0].dq_out = static_cast<uint8_t*>(full_out) + (size_t)(segs[c->rank].global_start - segs[0].global_start) * osz;
+    q[0].dq_out = own_out;
     dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;
     dq.dq_nocodes = c->world == 1 ? 1 : 0;  // world 1: the fused dequant is the only reader
   }
@@ -1043,11 +1049,6 @@ qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, c
     js.length = segs[p].length;
     js.out = static_cast<uint8_t*>(full_out) + (size_t)(segs[p].global_start - segs[0].global_start) * osz;
     d.push_back(js);
-  }
-  if (fused_cfg_ok(c, cfg, in_dtype)) {
-    bool launched = false;
-    st = try_fused(c, q, d, cfg, 0, 1, out_dtype, s, dq, launched);
-    if (st != QSDP_OK || launched) return st;
   }
   // 1. quantize this rank's shard (and push it when `push`)
   st = run_quantize(q, in_dtype, cfg, nullptr, s, dq, lv ? c->wlevels : nullptr, c->wnlevels);
@@ -1076,7 +1077,9 @@ static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int3
                                        const qsdp_segment* segs, const qsdp_key* key, void* shard_out,
                                        int32_t out_dtype, void* stream, void* x_shard, const qsdp_lattice* lat) {
   if (c == nullptr || key == nullptr) return fail(QSDP_EINVAL, "null argument");
-  qsdp_status st = check_segs(c, segs);
+  qsdp_status st = comm_failed(c);
+  if (st != QSDP_OK) return st;
+  st = check_segs(c, segs);
   if (st != QSDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const qsdp_qcfg* cfg = &c->g;
@@ -1104,14 +1107,10 @@ static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int3
   d[0].length = segs[c->rank].length;
   d[0].out = shard_out;
   d[0].lat_x = x_shard;
-  if (lat == nullptr && fused_cfg_ok(c, cfg, in_dtype)) {
-    bool launched = false;
-    st = try_fused(c, q, d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 1), launched);
-    if (st != QSDP_OK || launched) return st;
-  }
   DynSrc dq = comm_dyn(c, 1);
   // world 1: the average of one source is the quantizer's own dequant epilogue (0.0 + v)
-  const bool fdq1 = c->world == 1 && lat == nullptr && shard_out != nullptr && fdq_ok(cfg, in_dtype, out_dtype);
+  const bool fdq1 = c->world == 1 && lat == nullptr && shard_out != nullptr && fdq_ok(cfg, in_dtype, out_dtype) &&
+                    aligned(shard_out, dtype_size(out_dtype) == 2 ? 8 : 16);
   if (fdq1) {
     q[0].dq_out = shard_out;
     dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;

@@ -261,15 +261,6 @@ struct DJobTable {
   const unsigned long long* lat_step_ptr;
 };
 
-// Synchronisation words of a fused single-launch collective (see fused_collective_kernel).
-struct FuseSync {
-  unsigned long long* epoch;                       // local: collectives completed
-  unsigned int* arrive;                            // local: CTAs arrived in this launch
-  unsigned long long* go;                          // local: grid release flag (= target)
-  unsigned long long* flags[QSDP_FUSE_MAX_WORLD];  // flags[j] = rank j's flag array
-  int rank, world;
-};
-
 // Geometry of one wire message (qsdp_wire.cu).
 struct WireGeom {
   int64_t length;      // total elements

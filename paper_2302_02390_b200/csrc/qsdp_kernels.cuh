@@ -1905,62 +1905,6 @@ __global__ void __launch_bounds__(256) dequant_lat_fast_kernel(const __grid_cons
 }
 
 // ---------------------------------------------------------------------------
-// C1 / C2 as ONE persistent kernel per collective:
-//   phase A  quantize this rank's segments into its local slot(s) (TMA pipeline)
-//   barrier  grid-wide arrival (atomic counter) + cross-GPU flags over NVLink:
-//            the last CTA to arrive publishes `target` to every peer
-//            (st.release.sys), waits for all peers (ld.acquire.sys), advances the
-//            device epoch and releases the grid (go flag)
-//   phase C  pull-dequantize (C1) or ordered dequant-accumulate (C2) straight
-//            from the peers' slots over NVLink.
-// The grid is exactly the co-resident CTAs (persistent), so the in-kernel barrier
-// cannot deadlock.  World 1 uses the same kernel (grid barrier only).
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void fused_barrier(const FuseSync& fs, unsigned long long target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();  // this CTA's phase-A codes are visible to peers and other CTAs
-    const unsigned int prev = atomicAdd(fs.arrive, 1u);
-    if (prev == gridDim.x - 1) {
-      *reinterpret_cast<volatile unsigned int*>(fs.arrive) = 0u;  // everyone arrived: reset for next launch
-      for (int j = 0; j < fs.world; ++j) {
-        if (j == fs.rank) continue;
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fs.flags[j] + fs.rank), "l"(target) : "memory");
-      }
-      for (int j = 0; j < fs.world; ++j) {
-        if (j == fs.rank) continue;
-        unsigned long long v = 0;
-        do {
-          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(fs.flags[fs.rank] + j) : "memory");
-        } while (v < target);
-      }
-      *reinterpret_cast<volatile unsigned long long*>(fs.epoch) = target;
-      __threadfence();
-      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(fs.go), "l"(target) : "memory");
-    } else {
-      unsigned long long v = 0;
-      do {
-        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(fs.go) : "memory");
-      } while (v < target);
-    }
-  }
-  __syncthreads();
-}
-
-template <typename T, int INNER, int BITS, int NST, bool ACC, int OUT>
-__global__ void __launch_bounds__(256, 2) fused_collective_kernel(const __grid_constant__ QJobTable qt,
-                                                                  const __grid_constant__ DJobTable dt,
-                                                                  const __grid_constant__ FuseSync fs) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const unsigned long long target = ld_dev_u64(fs.epoch) + 1ull;
-  quantize_tma32_body<T, INNER, BITS, NST, 3>(qt, smem);
-  fused_barrier(fs, target);
-  // the phase-A ring is free again: reuse its start for the per-source scale rows
-  dequant_body<BITS, 32, OUT, true, ACC, true>(dt, reinterpret_cast<double*>(smem));
-}
-
-// ---------------------------------------------------------------------------
 // Host-side launch helpers (instantiated per translation unit).
 // ---------------------------------------------------------------------------
 inline int team_lanes(int S) {
@@ -1995,6 +1939,21 @@ inline int persistent_grid(F kern, int threads, size_t smem, int64_t total_bucke
   return grid_for(total_buckets, teams_per_warp, sms, threads / 32, per_sm);
 }
 
+// Opt a kernel into more than 48 KB of dynamic shared memory.  The attribute is
+// per device context, so the cache (one per kernel instantiation, passed in) is
+// indexed by the current device.
+template <typename F>
+inline cudaError_t ensure_smem_attr(F kern, size_t smem, size_t (&cache)[64]) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  size_t& done = cache[dev & 63];
+  if (smem <= done || smem <= 48 * 1024) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done = smem;
+  return e;
+}
+
 // Fast TMA path.  Returns false when the configuration needs the general kernel.
 template <typename T, int INNER, int BITS, int FDQ>
 cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
@@ -2005,12 +1964,8 @@ cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
   const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t) +
                       (size_t)wpc * 32 * sizeof(SeedOut);
   auto kern = quantize_tma32_kernel<T, INNER, BITS, NST, FDQ>;
-  static thread_local size_t smem_set = 0;  // per instantiation: set once, not during graph capture
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
+  static thread_local size_t smem_set[64] = {};  // per instantiation and device
+  if (cudaError_t e = ensure_smem_attr(kern, smem, smem_set); e != cudaSuccess) return e;
   const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, 1, sms);
   kern<<<grid, wpc * 32, smem, s>>>(tab);
   return cudaGetLastError();
@@ -2040,12 +1995,8 @@ cudaError_t launch_q_tma(const QJobTable& tab, bool vec, int sms, cudaStream_t s
     while (wpc > 1 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
     const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t);
     auto kern = quantize_tma_kernel<T, INNER, BITS, TL, NST>;
-    static thread_local size_t smem_set = 0;
-    if (smem > smem_set) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      smem_set = smem;
-    }
+    static thread_local size_t smem_set[64] = {};
+    if (cudaError_t e = ensure_smem_attr(kern, smem, smem_set); e != cudaSuccess) return e;
     const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, TEAMS, sms);
     kern<<<grid, wpc * 32, smem, s>>>(tab, vec ? 1 : 0);
     return cudaGetLastError();

@@ -611,9 +611,8 @@ template <typename T, int G, int BITS>
 static void launch_hold_b(const QJobTable& tab, const double* levels, int nl, int sms, cudaStream_t s) {
   auto k = quantize_levels_hold_kernel<T, G, BITS>;
   const size_t sm = level_index_smem(nl);
-  static thread_local size_t attr = 48 * 1024;  // opt in above the default once per instantiation
-  if (sm > attr && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess)
-    attr = sm;
+  static thread_local size_t attr[64] = {};  // opt in above the default once per instantiation and device
+  ensure_smem_attr(k, sm, attr);
   k<<<persistent_grid(k, 256, sm, tab.total_buckets, 1, sms), 256, sm, s>>>(tab, levels, nl);
 }
 

@@ -48,10 +48,6 @@ class QSDPContext:
         # table (levels.LevelTable, e.g. levels.learn_weight_levels(model weights))
         self.ag = QSDPComm(max_shard_numel, wspec, gspec, group=group, device=device, weight_levels=weight_levels)
         self.rs = QSDPComm(max_shard_numel, wspec, gspec, group=group, device=device)
-        # the two streams run collectives concurrently: never the fused single-launch form,
-        # whose grid-wide barrier needs every CTA of the GPU resident
-        self.ag.set_fused(False)
-        self.rs.set_fused(False)
         # the comm streams overlap backward / forward compute: cap their SMs
         if sm_budget is None:
             import os

@@ -15,9 +15,6 @@ keyed stream ``bucket_rng(root, step, layer, PHASE_LATTICE, 0, 0)`` -- every ran
 draws the same lattice without communication (the single-process reference
 draws it from its sequential generator; ``qsdp_step(..., shift=r)`` with this r
 reproduces our result bit-for-bit for fp64 iterates, tests/test_gpu_lattice.py).
-
-Also mirrored: the plan derivations ``derive_eta`` / ``derive_grid`` /
-``derive_T`` (optimizer.py:45-94), host scalar arithmetic.
 """
 
 from __future__ import annotations
@@ -31,11 +28,9 @@ import torch
 from . import _lib
 from .quantize import QuantSpec, SegmentKey, _DTYPE_CODE, _require_cuda, _stream
 
-__all__ = ["PHASE_LATTICE", "LatticeStep", "shift_key", "dequant_accumulate_lattice", "derive_eta", "derive_grid",
-           "derive_T"]
+__all__ = ["PHASE_LATTICE", "LatticeStep", "shift_key", "dequant_accumulate_lattice"]
 
 PHASE_LATTICE = 3
-_CEIL_GUARD = 1e-9
 
 
 def shift_key(root_seed: int, step: int, layer: int) -> SegmentKey:
@@ -83,44 +78,3 @@ def dequant_accumulate_lattice(sources, length: int, spec: QuantSpec, divisor: i
             g_out.data_ptr() if g_out is not None else None, _DTYPE_CODE[gdt], x.data_ptr(), ctypes.byref(lat),
             _stream(x.device)))
     return x
-
-
-def _iceil(x: float) -> int:
-    return int(math.ceil(x - _CEIL_GUARD))
-
-
-def derive_eta(epsilon: float, alpha: float, sigma_sq_total: float) -> float:
-    """Step-size factor min{(3/10) epsilon alpha / sigma^2, 1} (optimizer.py:45-55)."""
-    if epsilon <= 0:
-        raise ValueError(f"epsilon must be > 0, got {epsilon}")
-    if alpha <= 0:
-        raise ValueError(f"alpha must be > 0, got {alpha}")
-    if sigma_sq_total < 0:
-        raise ValueError("total gradient variance must be nonnegative")
-    if sigma_sq_total == 0:
-        return 1.0
-    return min(0.3 * epsilon * alpha / sigma_sq_total, 1.0)
-
-
-def derive_grid(eta: float, alpha: float, beta: float, delta_star: float) -> tuple[float, int]:
-    """Fine pitch delta = eta * delta_star / ceil(16 (beta/alpha)^2), ratio forced
-    integral (optimizer.py:58-77)."""
-    if not 0 < eta <= 1:
-        raise ValueError(f"eta must be in (0, 1], got {eta}")
-    if not 0 < alpha <= beta:
-        raise ValueError("need 0 < alpha <= beta")
-    if delta_star <= 0:
-        raise ValueError("delta_star must be > 0")
-    m = _iceil(16.0 * (beta / alpha) ** 2)
-    exact = m / eta
-    ratio = round(exact) if abs(exact - round(exact)) < 1e-9 else _iceil(exact)
-    return delta_star / ratio, ratio
-
-
-def derive_T(eta: float, alpha: float, beta: float, initial_gap: float, epsilon: float) -> int:
-    """Iteration count ceil((10/eta)(beta/alpha) ln(gap/epsilon)) (optimizer.py:80-89)."""
-    if epsilon <= 0:
-        raise ValueError("epsilon must be > 0")
-    if initial_gap <= epsilon:
-        return 0
-    return _iceil((10.0 / eta) * (beta / alpha) * math.log(initial_gap / epsilon))

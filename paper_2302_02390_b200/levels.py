@@ -8,7 +8,6 @@ Mirrors the reference's non-uniform codebook API (pkg/src/qsdp/quantize.py):
 * ``quantize_bucket(..., "levels", levels=table)``      quantize.py:235-286
   and ``dequantize(block, "levels", table)``            quantize.py:225-231
   (routed here from :mod:`.quantize`)
-* ``learned_vs_uniform_error``                          experiments.py:405-441
 
 Quantize / dequantize / learn run as sm_100a kernels behind the C ABI
 (``qsdp_quantize_levels*``, ``qsdp_dequantize_levels*``, ``qsdp_learn_levels``);
@@ -20,7 +19,6 @@ table, as the reference keeps it on the host.
 from __future__ import annotations
 
 import ctypes
-import math
 import warnings
 
 import numpy as np
@@ -30,7 +28,7 @@ from . import _lib
 from .quantize import QuantSpec, _DTYPE_CODE, _require_cuda, _stream, codes_bytes, num_buckets
 
 __all__ = ["LevelTable", "learn_levels", "quantize_with_levels", "quantize_levels", "quantize_levels_segments",
-           "dequantize_levels", "learned_vs_uniform_error", "normalize_buckets", "learn_weight_levels"]
+           "dequantize_levels", "learn_weight_levels"]
 
 
 class LevelTable:
@@ -203,30 +201,7 @@ def dequantize_levels(codes, meta, length: int, spec: QuantSpec, table: LevelTab
     return out
 
 
-def learned_vs_uniform_error(values, bit_width: int, bucket_size: int = 1024, passes: int = 1,
-                             learning_rate: float = 0.01):
-    """Relative L2 reconstruction error of uniform vs learned tables
-    (experiments.py:405-441), on the GPU: bucket-wise fp64 min-max
-    normalisation, ``passes`` learn_levels passes from the uniform table, then
-    nearest-level reconstruction on the original scale.  The two norms are
-    reduced on the device (summation order differs from numpy's: ~1e-15 rel)."""
-    x = _as_device_f64(values)
-    n = x.numel()
-    normalized, lo_e, span_e = normalize_buckets(x, bucket_size)
-    table = LevelTable.uniform(bit_width)
-    for _ in range(passes):
-        table = learn_levels(normalized, table, learning_rate)
-    uniform = LevelTable.uniform(bit_width)
-
-    def rel_err(tab):
-        q = tab.device(x.device)
-        recon = lo_e + q[quantize_with_levels(normalized, tab)] * span_e
-        return math.sqrt(float(((x - recon) ** 2).sum())) / math.sqrt(float((x * x).sum()))
-
-    return rel_err(uniform), rel_err(table), table
-
-
-def normalize_buckets(x: torch.Tensor, bucket_size: int):
+def _normalize_buckets(x: torch.Tensor, bucket_size: int):
     """Bucket-wise fp64 min-max normalisation as in experiments.py:418-426:
     returns (u, lo, span) per element, u = (x - lo) / span (0 where span == 0)."""
     x = x.reshape(-1).to(torch.float64)
@@ -249,7 +224,7 @@ def learn_weight_levels(tensors, bit_width: int, bucket_size: int = 1024, learni
     """A weight level table for the levels all-gather: the bucket-normalised
     values of ``tensors`` (a strided sample of at most ``max_values``), then
     ``passes`` learn_levels passes from the uniform table (Alg. 2)."""
-    us = [normalize_buckets(t.detach().reshape(-1), bucket_size)[0] for t in tensors if t.numel()]
+    us = [_normalize_buckets(t.detach().reshape(-1), bucket_size)[0] for t in tensors if t.numel()]
     u = torch.cat(us)
     if u.numel() > max_values:
         g = torch.Generator(device=u.device).manual_seed(seed)

@@ -1,7 +1,14 @@
-"""Multi-GPU check of QSDPComm (C1/C2 over NVLink peer memory); run with
+"""Multi-process check of QSDPComm (C1/C2 over peer memory); run with
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tests/dist_comm_check.py
 Every rank checks its all-gather output and its reduce-scatter shard bit-exactly
-against the oracle's single-process protocol (sharded.py:323-433)."""
+against the oracle's single-process protocol (sharded.py:323-433).
+
+QSDP_SAME_GPU=1 runs every rank on cuda:0 (gloo for the host plumbing: NCCL refuses
+two ranks on one device; QSDPComm only needs all_gather_object + barrier for the IPC
+handle exchange).  The data path is unchanged -- CUDA IPC mappings of the other
+processes' workspaces, the push mirror, the system-scope flag barrier, parity-slot
+reuse and the world>1 own-shard fused dequant -- so a one-GPU box exercises the
+whole multi-process protocol; only the links are HBM instead of NVLink."""
 
 import os
 import sys
@@ -16,21 +23,26 @@ from oracle import oracle as O  # noqa: E402  (checker only)
 from paper_2302_02390_b200.comm import QSDPComm, plan_segments  # noqa: E402
 from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey  # noqa: E402
 
+SAME_GPU = os.environ.get("QSDP_SAME_GPU", "0") == "1"
+
 
 def main():
-    dist.init_process_group("nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", 0 if SAME_GPU else local)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo" if SAME_GPU else "nccl")
     rank, world = dist.get_rank(), dist.get_world_size()
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
     failures = 0
-    cases = [(1 << 20, 1024, 8, 8, 1, True), (3 * 1024 * 1024 + 777, 1024, 8, 4, 1, True),
-             (1 << 22, 1024, 8, 8, 1024, True), (1 << 22, 1024, 8, 8, 1024, False), (50000, 64, 6, 4, 1, True),
-             (200000, 256, 4, 2, 256, True), (200000, 512, 16, 8, 1, False)]
-    for size, bucket, wb, gb, pad, fused in cases:
+    # (size, bucket, w bits, g bits, pad): pad 1 = shard_bounds, whose rank offsets are
+    # not multiples of 4 for the odd sizes (the own-shard fused dequant must then
+    # leave that shard to K3's scalar stores -- ADVICE r1)
+    cases = [(1 << 20, 1024, 8, 8, 1), (3 * 1024 * 1024 + 777, 1024, 8, 4, 1), (1000003, 1024, 8, 8, 1),
+             (1 << 22, 1024, 8, 8, 1024), (50000, 64, 6, 4, 1),
+             (200000, 256, 4, 2, 256), (200000, 512, 16, 8, 1)]
+    for size, bucket, wb, gb, pad in cases:
         segs = plan_segments(size, world, pad)
         maxseg = max(n for _, n in segs)
         comm = QSDPComm(maxseg, QuantSpec(wb, bucket, "shift"), QuantSpec(gb, bucket, "uniform_stochastic"))
-        comm.set_fused(fused)
         rng = np.random.default_rng(size)
         full = (rng.standard_normal(size) * 0.02).astype(np.float32)
         grads = [(np.random.default_rng(size + 1 + p).standard_normal(size) * 1e-3).astype(np.float32)
@@ -57,7 +69,7 @@ def main():
             ok_rs = np.array_equal(sh[:n].cpu().numpy(), (acc / world).astype(np.float32))
             if not (ok_ag and ok_rs):
                 failures += 1
-                print(f"rank {rank} size {size} fused {fused} step {step}: ag {ok_ag} rs {ok_rs}", flush=True)
+                print(f"rank {rank} size {size} step {step}: ag {ok_ag} rs {ok_rs}", flush=True)
         # graph capture of one AG + RS with the step read on the device (epoch on device too)
         from paper_2302_02390_b200.quantize import advance_counter
         ctr = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -97,13 +109,16 @@ def main():
                 failures += 1
                 print(f"rank {rank} size {size} graph replay {rep}: mismatch", flush=True)
         comm.close()
+    failures += offset_views(rank, world, dev)
     failures += levels_all_gather(rank, world, dev)
     failures += lattice_reduce_scatter(rank, world, dev)
     failures += pipelined(rank, world, dev)
-    t = torch.tensor([failures], device=dev)
+    failures += missed_barrier(rank, world, dev)
+    t = torch.tensor([failures], device="cpu" if SAME_GPU else dev)
     dist.all_reduce(t)
     if rank == 0:
-        print(f"dist_comm_check world={world}: {'OK' if t.item() == 0 else 'FAILED'}", flush=True)
+        print(f"dist_comm_check world={world}{' (all ranks on cuda:0)' if SAME_GPU else ''}: "
+              f"{'OK' if t.item() == 0 else 'FAILED'}", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if t.item() == 0 else 1)
 
@@ -186,6 +201,76 @@ def pipelined(rank, world, dev):
             print(f"rank {rank} pipelined size {size}: mismatch", flush=True)
         one.close()
         pipe.close()
+    return fails
+
+
+def offset_views(rank, world, dev):
+    """Outputs that are offset views (out[1:], shard[3:]) of larger buffers: no
+    alignment is assumed anywhere on the path."""
+    fails = 0
+    size, bucket = 777777, 1024
+    segs = plan_segments(size, world, 1)
+    comm = QSDPComm(max(n for _, n in segs), QuantSpec(8, bucket, "shift"), QuantSpec(8, bucket, "uniform_stochastic"))
+    full = (np.random.default_rng(7).standard_normal(size) * 0.02).astype(np.float32)
+    grads = [(np.random.default_rng(70 + p).standard_normal(size) * 1e-3).astype(np.float32) for p in range(world)]
+    s, n = segs[rank]
+    for step in range(2):
+        out_big = torch.full((size + 1,), float("nan"), device=dev)
+        comm.all_gather(torch.from_numpy(full[s:s + n]).to(dev), segs, SegmentKey(3, step, 2, 0, 0), out_big[1:])
+        exp = np.zeros(size)
+        for sq, nq in segs:
+            c, m, _ = O.quantize_segment(full[sq:sq + nq], sq, bucket, 8, 0, (3, step, 2, 0, 0), 8)
+            exp[sq:sq + nq] = O.dequantize_segment(c, m, nq, bucket, 8, 8)
+        ok_ag = np.array_equal(out_big[1:].cpu().numpy(), exp.astype(np.float32))
+        g_big = torch.zeros(size + 3, device=dev)
+        g_big[3:] = torch.from_numpy(grads[rank]).to(dev)
+        sh_big = torch.full((n + 1,), float("nan"), device=dev)
+        comm.reduce_scatter(g_big[3:], segs, SegmentKey(3, step, 2, 2, rank), sh_big[1:])
+        acc = np.zeros(n)
+        for p in range(world):
+            c, m, _ = O.quantize_segment(grads[p][s:s + n], s, bucket, 8, 1, (3, step, 2, 2, p), 8)
+            acc = acc + O.dequantize_segment(c, m, n, bucket, 8, 8)
+        ok_rs = np.array_equal(sh_big[1:].cpu().numpy(), (acc / world).astype(np.float32))
+        if not (ok_ag and ok_rs):
+            fails += 1
+            print(f"rank {rank} offset views step {step}: ag {ok_ag} rs {ok_rs}", flush=True)
+    comm.close()
+    return fails
+
+
+def missed_barrier(rank, world, dev):
+    """Failure detection: rank world-1 skips a collective; the others' barrier gives up
+    after the timeout and the communicator reports QSDP_EPEER instead of hanging."""
+    from paper_2302_02390_b200._lib import QSDPError
+    if world < 2:
+        return 0
+    fails = 0
+    size = 100000
+    segs = plan_segments(size, world, 1)
+    comm = QSDPComm(max(n for _, n in segs), QuantSpec(8, 1024, "shift"), QuantSpec(8, 1024, "uniform_stochastic"))
+    comm.set_timeout(1500)
+    s, n = segs[rank]
+    x = torch.randn(n, device=dev)
+    out = torch.empty(size, device=dev)
+    if rank != world - 1:
+        comm.all_gather(x, segs, SegmentKey(0, 0, 0, 0, 0), out)
+        torch.cuda.synchronize()
+        try:
+            comm.check()
+            fails += 1
+            print(f"rank {rank}: missed barrier not detected", flush=True)
+        except QSDPError as e:
+            if "did not arrive" not in str(e):
+                fails += 1
+                print(f"rank {rank}: unexpected error {e}", flush=True)
+        try:  # later collectives fail fast
+            comm.all_gather(x, segs, SegmentKey(0, 1, 0, 0, 0), out)
+            fails += 1
+            print(f"rank {rank}: collective after a failed barrier did not raise", flush=True)
+        except QSDPError:
+            pass
+    dist.barrier()
+    comm.close()
     return fails
 
 

@@ -115,32 +115,3 @@ def test_collective_ledger_records(oracle):
         assert e.reducescatter_bits == sum(m * (P - 1) for m in msg)
         assert e.allgather_payload_bits == sum(n * spec.bits * (P - 1) for _, n in segs)
         assert e.allgather_events == e.reducescatter_events == 1
-
-
-def test_lattice_plan_derivations():
-    """derive_eta / derive_grid / derive_T restate optimizer.py:45-89."""
-    import math
-    from paper_2302_02390_b200.lattice import derive_T, derive_eta, derive_grid
-    assert derive_eta(0.1, 1.0, 0.0) == 1.0
-    assert derive_eta(0.1, 0.5, 2.0) == min(0.3 * 0.1 * 0.5 / 2.0, 1.0)
-    d, ratio = derive_grid(0.5, 1.0, 2.0, 0.01)
-    assert ratio == math.ceil(16 * 4 / 0.5) and d == 0.01 / ratio
-    assert derive_T(1.0, 1.0, 1.0, 0.5, 1.0) == 0
-    assert derive_T(0.5, 1.0, 2.0, 10.0, 0.1) == math.ceil(20 * 2 * math.log(100) - 1e-9)
-    with pytest.raises(ValueError):
-        derive_grid(1.5, 1.0, 2.0, 0.01)
-
-
-@pytest.mark.reference
-def test_lattice_plan_matches_reference(reference):
-    from qsdp import optimizer as R
-    from paper_2302_02390_b200 import lattice as L
-    rng = np.random.default_rng(3)
-    for _ in range(200):
-        eps, alpha = float(rng.uniform(1e-3, 1)), float(rng.uniform(0.1, 1))
-        beta, var = alpha * float(rng.uniform(1, 4)), float(rng.choice([0.0, rng.uniform(0, 10)]))
-        eta = L.derive_eta(eps, alpha, var)
-        assert eta == R.derive_eta(eps, alpha, var)
-        assert L.derive_grid(eta, alpha, beta, 0.01) == R.derive_grid(eta, alpha, beta, 0.01)
-        gap = float(rng.uniform(0, 10))
-        assert L.derive_T(eta, alpha, beta, gap, eps) == R.derive_T(eta, alpha, beta, gap, eps)
