@@ -11,7 +11,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqsdp_b200.so")
+# QSDP_LIB_PATH: an experiment build of the same library (A/B runs); default the in-tree build
+LIB_PATH = os.environ.get("QSDP_LIB_PATH") or os.path.join(_HERE, "libqsdp_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 QSDP_OK = 0

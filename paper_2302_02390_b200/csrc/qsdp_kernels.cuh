@@ -570,8 +570,8 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
 //    fq in {d_hi, d_hi+1} or fq == 0 off the bucket's extrema; those elements
 //    are recomputed with the exact __ddiv_rn chain.
 // ---------------------------------------------------------------------------
-// COH: codes written earlier in the same launch (fused collectives) or by a
-// peer -- read at L2 (ld.global.cg), never through the non-coherent path.
+// COH: codes written by a peer in flight -- read at L2 (ld.global.cg), never
+// through the non-coherent path.
 template <int BITS, bool COH = false>
 __device__ __forceinline__ uint64_t load_group_direct(const uint8_t* __restrict__ p, int gi) {
   if constexpr (COH) {

@@ -24,6 +24,7 @@ shard = torch.empty(n, device=dev)
 comm = QSDPComm(n, QuantSpec(8, 1024, "shift"), QuantSpec(8, 1024, "uniform_stochastic"), device=dev)
 for r in range(a.reps):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda._sleep(4_000_000)  # GPU busy while the host enqueues: the events time the kernels, not the launches
     ev[0].record()
     comm.all_gather(x, [(0, n)], SegmentKey(0, r, 0, 0, 0), full)
     ev[1].record()
