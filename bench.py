@@ -73,6 +73,13 @@ def parse():
     ap.add_argument("--no-levels", action="store_true", help="skip the learned-levels kernel timings")
     ap.add_argument("--serial", action="store_true",
                     help="one stream for every collective (default: FSDP2's schedule, RS on its own stream/comm)")
+    ap.add_argument("--inflight", type=int, default=2,
+                    help="collectives of one kind in flight (streams + communicators per kind; FSDP2 prefetch depth)")
+    ap.add_argument("--fwd-ag-sms", type=int, default=0, help="SM budget of the forward all-gathers (0 = all)")
+    ap.add_argument("--bwd-ag-sms", type=int, default=0, help="SM budget of the backward all-gathers (0 = all)")
+    ap.add_argument("--rs-sms", type=int, default=0, help="SM budget of the reduce-scatters (0 = all)")
+    ap.add_argument("--trace", default="", help="write the GPU timeline of one step replay (CUPTI via "
+                    "torch.profiler: every kernel's start / end / stream) and its overlap summary to this JSON file")
     ap.add_argument("--gpt-steps", type=int, default=8)
     ap.add_argument("--gpt-batch", type=int, default=8, help="sequences per GPU")
     ap.add_argument("--gpt-seq", type=int, default=1024)
@@ -176,34 +183,127 @@ def run_cpu_baseline(args, world, min_seconds=10.0):
                       f"{el:.1f} s wall, C oracle (oracle/qsdp_oracle.c) on {threads} threads"}
 
 
+def reference_workload(model, world):
+    """The B200 arm's step workload on the host: every dense FSDP group's weights and P virtual
+    ranks' gradients (rank p's gradient is a rotation of one N(0, 1e-3^2) draw -- the timing
+    does not depend on the values).  The simulated RS does P x the quantization work of P = 1
+    (every rank quantizes its whole gradient), so for world > 2 the step is a bounded sample
+    -- the leading groups up to 4/(2+P) of the parameters -- to keep the run within minutes."""
+    import numpy as np
+    from paper_2302_02390_b200.gpt import dense_groups
+    groups = dense_groups(model)
+    if world > 2:
+        total, keep, acc = sum(g.numel for g in groups), [], 0
+        for g in groups:
+            if acc >= total * 4.0 / (2 + world):
+                break
+            keep.append(g)
+            acc += g.numel
+        groups = keep
+    rng = np.random.default_rng(0)
+    work = []
+    for g in groups:
+        w = (rng.standard_normal(g.numel, dtype=np.float32) * np.float32(0.02))
+        base = rng.standard_normal(g.numel, dtype=np.float32) * np.float32(1e-3)
+        grads = [np.roll(base, 7919 * p) for p in range(world)]
+        work.append((w, grads))
+    return groups, work
+
+
 def run_reference(args):
+    """The reference's CPU implementation of the path (the C oracle port of sharded.py:323-433 /
+    quantize.py / wire.py, every host thread) on the B200 arm's own config: per step, AG fwd +
+    AG bwd + RS over every dense group of the model at P = world virtual ranks (the reference is
+    a single-process simulation of all P ranks)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     from oracle import oracle as O
     threads = len(os.sched_getaffinity(0))
-    _, n, w, grads = cpu_sample(args.model, world)
-    for s in range(args.warmup):
-        cpu_protocol_step(O, w, grads, world, args.wbits, args.gbits, args.bucket, s, threads)
+    from paper_2302_02390_b200.gpt import dense_groups
+    all_groups = dense_groups(args.model)
+    groups, work = reference_workload(args.model, world)
+    n_total = sum(g.numel for g in groups)
+    full = len(groups) == len(all_groups)
+    warm = min(args.warmup, 1)  # host code: one warm-up step pages the arrays in
+
+    def step(s):
+        for li, (w, grads) in enumerate(work):
+            O.gather(w, world, args.bucket, args.wbits, 0, s, li, 0, threads)
+            O.gather(w, world, args.bucket, args.wbits, 0, s, li, 1, threads)
+            O.reduce_scatter(grads, args.bucket, args.gbits, 0, s, li, threads)
+
+    for s in range(warm):
+        step(s)
     t0 = time.perf_counter()
     for s in range(args.steps):
-        cpu_protocol_step(O, w, grads, world, args.wbits, args.gbits, args.bucket, s, threads)
+        step(warm + s)
     el = time.perf_counter() - t0
-    value = world * 12.0 * n * args.steps / el / 1e9
+    value = world * 12.0 * n_total * args.steps / el / 1e9
     line = {
         "impl": "reference", "metric": "quantized all-gather+reduce-scatter effective GB/s", "value": round(value, 4),
-        "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": warm,
         "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.model} QSDP w{args.wbits}/g{args.gbits} bucket {args.bucket}: AG fwd + AG bwd "
-                               f"+ RS, bounded sample of {n} elements per step, P={world} virtual ranks on the host"},
+        "config": bench_config(args, world, len(all_groups), sum(g.numel for g in all_groups)),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{n} elements per step (first block group / P), oracle/qsdp_oracle.c"},
+                         "sample": ("the full step" if full else f"a bounded sample of the step (the leading "
+                                                                   f"{len(groups)} of {len(all_groups)} groups)")
+                                   + f": AG fwd + AG bwd + RS over {n_total} elements at P={world} virtual "
+                                     f"ranks, oracle/qsdp_oracle.c on {threads} threads"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def trace_step(g, flush, path):
+    """Timeline of one step-graph replay (after an L2 flush): CUPTI kernel records through
+    torch.profiler, reduced to per-kernel intervals and the overlap between streams
+    (no nsys in this image)."""
+    import tempfile
+
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    flush.fill_(7)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        g.replay()
+        torch.cuda.synchronize()
+    with tempfile.NamedTemporaryFile(suffix=".json") as f:
+        prof.export_chrome_trace(f.name)
+        tr = json.load(open(f.name))
+    ks = [e for e in tr.get("traceEvents", []) if e.get("ph") == "X" and e.get("cat") == "kernel"]
+    ks.sort(key=lambda e: e["ts"])
+    t0 = ks[0]["ts"] if ks else 0.0
+    rec = [{"name": e["name"][:90], "stream": e.get("args", {}).get("stream"), "start_us": round(e["ts"] - t0, 2),
+            "end_us": round(e["ts"] + e["dur"] - t0, 2)} for e in ks]
+    # union of busy time, and the time with >= 2 kernels running
+    pts = sorted([(r["start_us"], 1) for r in rec] + [(r["end_us"], -1) for r in rec])
+    busy = multi = 0.0
+    depth, last = 0, None
+    for t, d in pts:
+        if last is not None and depth > 0:
+            busy += t - last
+            if depth > 1:
+                multi += t - last
+        depth += d
+        last = t
+    summ = {"kernels": len(rec), "span_us": round(rec[-1]["end_us"], 2) if rec else 0.0,
+            "sum_kernel_us": round(sum(r["end_us"] - r["start_us"] for r in rec), 2), "busy_us": round(busy, 2),
+            "overlapped_us": round(multi, 2), "streams": sorted({str(r["stream"]) for r in rec}),
+            "how": "torch.profiler (CUPTI) of one replay of the timed step graph; times relative to the first kernel"}
+    json.dump({"summary": summ, "kernels": rec}, open(path, "w"), indent=1)
+    print(f"trace: {summ}", file=sys.stderr, flush=True)
+
+
+def bench_config(args, world, ngroups, n_total):
+    """The workload both arms report (the reference arm runs the same step on the host)."""
+    return {"workload": f"{args.model} QSDP w{args.wbits}/g{args.gbits} bucket {args.bucket}: per step "
+                        f"AG fwd + AG bwd + RS over {ngroups} FSDP groups ({n_total} dense params)",
+            "out_dtype": args.out_dtype, "quantizer_input": "f32", "arithmetic": "f64 (bit-exact)",
+            "parallelism": f"qsdp{world}", "convention": "sum over ranks of 4*N per collective / time"}
 
 
 # ---------------------------------------------------------------------------
@@ -264,14 +364,22 @@ def main():
         state.append(st)
     flush = torch.empty(64 << 20, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
     step_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
-    comm = QSDPComm(max_seg, wspec, gspec, device=dev)
-    comm.set_step_source(step_ctr)
-    # FSDP2's schedule (fsdp.QSDPContext): reduce-scatters on their own stream with their own
-    # communicator, RS(i) after AG(i)'s backward re-gather, overlapping AG(i-1)
-    rs_comm = comm if args.serial else QSDPComm(max_seg, wspec, gspec, device=dev)
-    rs_comm.set_step_source(step_ctr)
-    rs_stream = torch.cuda.Stream(device=dev)
+    # FSDP2's schedule (fsdp.QSDPContext): all-gathers on one stream, reduce-scatters on their
+    # own stream with their own communicator, RS(i) after AG(i)'s backward re-gather, overlapping
+    # AG(i-1).  --inflight K keeps K collectives of each kind in flight (K streams and
+    # communicators per kind, round robin: FSDP2's prefetch depth), so one collective's tail
+    # overlaps the next one's ramp; --*-sms split the SMs between the overlapping kinds.
+    K = max(1, args.inflight)
     stream = torch.cuda.current_stream(dev)
+    ag_comms = [QSDPComm(max_seg, wspec, gspec, device=dev) for _ in range(K)]
+    rs_comms = ag_comms if args.serial else [QSDPComm(max_seg, wspec, gspec, device=dev) for _ in range(K)]
+    for c in set(ag_comms + rs_comms):
+        c.set_step_source(step_ctr)
+    comm, rs_comm = ag_comms[0], rs_comms[0]
+    # all-gather slot 0 runs on the issuing stream (the capture stream inside a graph)
+    ag_side = [torch.cuda.Stream(device=dev) for _ in range(K - 1)]
+    rs_side = [torch.cuda.Stream(device=dev) for _ in range(K)]
+    rs_stream = rs_side[0]
 
     # ---- the step as a list of launches (kind, bytes, fn) ----
     kinds = ("K1_quantize_shift", "K3_dequantize", "K2_quantize_stochastic", "K4_dequant_accumulate")
@@ -304,36 +412,54 @@ def main():
         return L
 
     def comm_launches():
-        """The step's collectives: (kind, launches, fn, on_rs_stream)."""
+        """The step's collectives: (kind, launches, fn, slot, after): slot = the stream /
+        communicator index within the kind; `after` = index of the launch it must follow."""
         L = []
         per = 3 if world > 1 else 2  # quantize (+ barrier) + dequant
+        j = 0
         for gi, st in enumerate(state):
-            L.append(("AG", per, lambda st=st, gi=gi: comm.all_gather(
-                st["shard"], st["segs"], SegmentKey(0, 0, gi, 0, 0), st["full"]), False))
+            c = ag_comms[j % K]
+            L.append(("AG", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.fwd_ag_sms), c.all_gather(
+                st["shard"], st["segs"], SegmentKey(0, 0, gi, 0, 0), st["full"])), ("ag", j % K), None))
+            j += 1
+        r = 0
         for gi in range(len(state) - 1, -1, -1):
             st = state[gi]
-            L.append(("AG", per, lambda st=st, gi=gi: comm.all_gather(
-                st["shard"], st["segs"], SegmentKey(0, 0, gi, 1, 0), st["full"]), False))
-            L.append(("RS", per, lambda st=st, gi=gi: rs_comm.reduce_scatter(
-                st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"]), not args.serial))
+            c = ag_comms[j % K]
+            L.append(("AG", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.bwd_ag_sms), c.all_gather(
+                st["shard"], st["segs"], SegmentKey(0, 0, gi, 1, 0), st["full"])), ("ag", j % K), None))
+            j += 1
+            c = rs_comms[r % K]
+            L.append(("RS", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.rs_sms), c.reduce_scatter(
+                st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"])),
+                ("ag" if args.serial else "rs", (r if args.serial else r) % K), len(L) - 1))
+            r += 1
         return L
 
     def issue(launches):
-        """Issue a step's collectives on the current stream (+ the RS stream, joined at the end)."""
+        """Issue a step's collectives on their streams (forked from and joined to the current stream)."""
         main = torch.cuda.current_stream(dev)
-        forked = False
-        for _, _, fn, on_rs in launches:
-            if on_rs:
-                ev = torch.cuda.Event()
-                ev.record(main)
-                rs_stream.wait_event(ev)
-                with torch.cuda.stream(rs_stream):
-                    fn()
-                forked = True
-            else:
+        ag_streams = [main] + ag_side
+        rs_streams = ag_streams if args.serial else rs_side
+        used = {id(main)}
+        start = torch.cuda.Event()
+        start.record(main)
+        done = {}
+        for idx, (_, _, fn, (kind, slot), after) in enumerate(launches):
+            s_ = (ag_streams if kind == "ag" else rs_streams)[slot]
+            if id(s_) not in used:
+                s_.wait_event(start)
+                used.add(id(s_))
+            if after is not None:
+                s_.wait_event(done[after])
+            with torch.cuda.stream(s_):
                 fn()
-        if forked:
-            main.wait_stream(rs_stream)
+            ev = torch.cuda.Event()
+            ev.record(s_)
+            done[idx] = ev
+        for s_ in set(ag_streams + rs_streams):
+            if s_ is not main and id(s_) in used:
+                main.wait_stream(s_)
 
     # `value` times the product path (the communicator); the per-kernel roofline graphs replay
     # the same kernels through the batch API.
@@ -412,6 +538,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
+    if args.trace and rank == 0:
+        trace_step(g_step, flush, args.trace)
     value = world * 12.0 * N_total / (ms_step * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel: per-kind graphs timed with CUDA events ----
@@ -443,7 +571,7 @@ def main():
         osz = 4 if out_dt == torch.float32 else 2
         fused_kinds = {}
         for kind, sel in (("AG_K1_fused_dequant", "AG"), ("RS_K2_fused_dequant", "RS")):
-            fns = [x[2] for x in launches if x[0] == sel]
+            fns = [x[2] for x in launches if x[0] == sel]  # serial on one stream: the kernels' own throughput
             gk = capture(lambda fns=fns: [f() for f in fns], keep=True)
             cnt = kernel_nodes(gk) or len(fns)
             if cnt != len(fns):  # not fused for this config: keep the standalone breakdown
@@ -613,6 +741,8 @@ def main():
         bi = sum(h["shard"].numel() * 4 + h["grad"].numel() * 4 for h in host)
         bo = sum(st["n"] * 4 for st in state)
         h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        comm.set_sm_budget(0)  # the e2e step is PCIe-bound: full-GPU collectives
+        rs_comm.set_sm_budget(0)
         # The last gradient of the backward order streams through in bucket-aligned chunks
         # (H2D -> RS -> D2H per chunk), so its result copy does not wait for the whole gradient:
         # only the final chunk's D2H is left after the last H2D byte.  Same codes and results
@@ -742,22 +872,22 @@ def main():
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.model} QSDP w{args.wbits}/g{args.gbits} bucket {args.bucket}: per step "
-                                   f"AG fwd + AG bwd + RS over {len(groups)} FSDP groups ({N_total} dense params)",
-                       "out_dtype": args.out_dtype, "quantizer_input": "f32", "arithmetic": "f64 (bit-exact)",
-                       "l2": "256 MB L2 flush between timed steps; per-step working set > 126 MB L2",
-                       "parallelism": f"qsdp{world}", "execution": "one CUDA graph per step (device step counter), "
-                                    + ("quantize + barrier + dequantize launches per collective" if world > 1
-                                       else "one quantizer launch (fused dequant) per collective"),
-                       "convention": "sum over ranks of 4*N per collective / time"},
+            "config": dict(bench_config(args, world, len(groups), N_total), **{
+                "l2": "256 MB L2 flush between timed steps (outside the events: the step then pays the "
+                      "write-back of the flush's dirty lines in place of its own trailing ones); per-step "
+                      "working set 3 GB > 126 MB L2",
+                "execution": "one CUDA graph per step (device step counter), "
+                             + ("quantize + barrier + dequantize launches per collective" if world > 1
+                                else "one quantizer launch (fused dequant) per collective")
+                             + f"; {K} collectives of each kind in flight (FSDP2 prefetch depth; streams + "
+                               "communicators per kind), RS(i) after AG_bwd(i)"}),
             "roofline": roofline, "kernels": kernels, "kernels_unfused": kernels_unfused if world == 1 else None, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
             "levels": levels, "wire": wire, "lattice": lattice,
             "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
-    comm.close()
-    if rs_comm is not comm:
-        rs_comm.close()
+    for c in set(ag_comms + rs_comms):
+        c.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -783,25 +783,29 @@ __device__ __forceinline__ U128 shfl_u128(const U128& v, int src) {
   return r;
 }
 
-// Cached job lookup: a warp walks buckets in increasing order, so the job
-// index only moves forward; re-scan only when the bucket leaves the cached job.
-struct JobCursor {
+// Stateless job lookup for the TMA32 quantizer: one-job tables (every collective)
+// resolve without a search, larger ones by binary search over the (param-space)
+// bucket_base prefix.  Keeping no cursor state across buckets spares registers
+// the per-bucket prologue would otherwise spill (ncu r2: LDL reloads of a cached
+// cursor stalled ~9% of K2's samples on long scoreboard).
+__device__ __forceinline__ BucketRef resolve_fast(const QJobTable& tab, int64_t b, int S) {
   int j = 0;
-  int64_t lo = 0, hi = -1;  // bucket range [lo, hi) of job j
-  __device__ __forceinline__ BucketRef get(const QJobTable& tab, int64_t b, int S) {
-    if (b < lo || b >= hi) {
-      j = find_job_q(tab, b);
-      lo = tab.jobs[j].bucket_base;
-      hi = j + 1 < tab.njobs ? tab.jobs[j + 1].bucket_base : tab.total_buckets;
+  if (tab.njobs > 1) {
+    int lo = 0, hi = tab.njobs - 1;  // last job with bucket_base <= b
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tab.jobs[mid].bucket_base <= b) lo = mid;
+      else hi = mid - 1;
     }
-    BucketRef r;
-    r.j = j;
-    r.lb = b - lo;
-    r.off = r.lb * S;
-    r.n = (int)min((int64_t)S, tab.jobs[j].length - r.off);
-    return r;
+    j = lo;
   }
-};
+  BucketRef r;
+  r.j = j;
+  r.lb = b - tab.jobs[j].bucket_base;
+  r.off = r.lb * S;
+  r.n = (int)min((int64_t)S, tab.jobs[j].length - r.off);
+  return r;
+}
 
 template <typename T, int INNER, int BITS, int NST, int FDQ = 0>
 __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_t* smem) {
@@ -818,10 +822,19 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
   // lane-parallel seeds of the warp's next 32 buckets live in shared memory
   SeedOut* seeds = reinterpret_cast<SeedOut*>(smem + (size_t)wpc * NST * S * sizeof(T) +
                                               (size_t)wpc * NST * sizeof(uint64_t)) + wib * 32;
+  // stochastic octet path: the per-lane jump A_{8 lane+1}, G_{8 lane+1} and the octet stride
+  // A_{249}, G_{249}, copied once per CTA from the global table (a per-bucket LDG of them was
+  // a long-scoreboard stall)
+  JumpEntry* sjump = reinterpret_cast<JumpEntry*>(reinterpret_cast<uint8_t*>(seeds - wib * 32) +
+                                                  (size_t)wpc * 32 * sizeof(SeedOut));
+  if (INNER == 1) {
+    for (int t = threadIdx.x; t <= 32; t += blockDim.x) sjump[t] = g_jump[t < 32 ? 8 * t + 1 : 8 * 32 - 7];
+    __syncthreads();
+  }
   const int64_t gw = (int64_t)blockIdx.x * wpc + wib;
   const int64_t nw = (int64_t)gridDim.x * wpc;
   const int64_t total = tab.total_buckets;
-  const int64_t pbs = payload_bytes(S, BITS);
+  constexpr int PB8 = BITS;  // payload bytes per 8 elements: pbs = S * BITS / 8 (S % 8 == 0 here)
   const int gl = (S / 4 + 31) / 32;
   const double top = (double)TOP;
   const double pitch = __ddiv_rn(1.0, top);
@@ -836,14 +849,13 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
   __syncwarp();
 
   auto bucket_of = [&](int64_t k) { return gw + k * nw; };
-  JobCursor icur, mcur;
   auto issue = [&](int64_t k) {
     if (lane == 0) {
       const int64_t b = bucket_of(k);
       uint64_t* bar = &bars[k % NST];
       uint32_t bytes = 0;
       const T* src = nullptr;
-      const BucketRef br = icur.get(tab, b, S);
+      const BucketRef br = resolve_fast(tab, b, S);
       if (br.n == S) {
         src = reinterpret_cast<const T*>(tab.jobs[br.j].x) + br.off;
         if (((uintptr_t)src & 15u) == 0) bytes = (uint32_t)(S * sizeof(T));
@@ -863,7 +875,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
     }
     const int stage = (int)(k % NST);
     const int64_t b = bucket_of(k);
-    const BucketRef br = mcur.get(tab, b, S);
+    const BucketRef br = resolve_fast(tab, b, S);
     const QJob& J = tab.jobs[br.j];
     const int n = br.n;
     const T* gx = reinterpret_cast<const T*>(J.x) + br.off;
@@ -947,7 +959,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
     const double r = INNER == 0 ? sd.r : 0.0;
     const U128 s0 = INNER == 1 ? sd.s0 : U128{0, 0};
     const U128 inc = INNER == 1 ? sd.inc : U128{0, 0};
-    uint8_t* cbase = J.codes + poff + br.lb * pbs;
+    uint8_t* cbase = J.codes + poff + br.lb * (int64_t)(S / 8 * PB8);
     const double lo = (double)lof;
     const double span = __dsub_rn((double)hif, lo);
     float shift_f = 0.0f;
@@ -1040,9 +1052,9 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
         // octets: lane owns 8 consecutive elements 8*o (o = lane, lane+32, ...), so the
         // stream jumps once per 8 draws (by 256-7) instead of once per 4.
         // jump constants from the (L1-resident) table, per bucket: keeps registers for the loop
-        const JumpEntry o0 = g_jump[8 * lane + 1];
+        const JumpEntry o0 = sjump[lane];
         U128 st = add128(mul128(o0.a, s0), mul128(o0.g, inc));  // state_{8*lane+1}
-        const JumpEntry oj = g_jump[8 * 32 - 7];
+        const JumpEntry oj = sjump[32];
         const U128 OJa = oj.a;
         const U128 jc = mul128(oj.g, inc);
         const FusedDq fqs = fused_dq<FDQ>(tab, J, br.off, lof, hif, 0.0f, BITS);
@@ -1962,7 +1974,7 @@ cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
   int wpc = 8;
   while (wpc > 2 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
   const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t) +
-                      (size_t)wpc * 32 * sizeof(SeedOut);
+                      (size_t)wpc * 32 * sizeof(SeedOut) + (INNER == 1 ? 33 * sizeof(JumpEntry) : 0);
   auto kern = quantize_tma32_kernel<T, INNER, BITS, NST, FDQ>;
   static thread_local size_t smem_set[64] = {};  // per instantiation and device
   if (cudaError_t e = ensure_smem_attr(kern, smem, smem_set); e != cudaSuccess) return e;
