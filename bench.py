@@ -655,6 +655,39 @@ def main():
                             "frac_of_hbm_peak": round(lbytes[name] / (tk * 1e-3) / 1e9 / hbm_peak, 4),
                             "bytes_per_pass": lbytes[name], "launches_per_pass": len(state)}
 
+    # ---- counter-based noise (QSDP_NOISE_PHILOX4x64): K1 / K2 with numpy's Philox4x64-10 ----
+    philox = None
+    if world == 1 and not args.no_levels:
+        pws = QuantSpec(args.wbits, args.bucket, "shift", "philox")
+        pgs = QuantSpec(args.gbits, args.bucket, "uniform_stochastic", "philox")
+
+        def pq_w():
+            for gi, st in enumerate(state):
+                quantize_segments([(st["shard"], 0, SegmentKey(0, 0, gi, 0, 0))], pws, out=[st["wq"]])
+
+        def pq_g():
+            for gi, st in enumerate(state):
+                quantize_segments([(st["grad"], 0, SegmentKey(0, 0, gi, 2, 0))], pgs, out=[st["gq"]])
+
+        pbytes = {"K1_quantize_shift_philox": sum(4 * st["n"] + codes_bytes(st["n"], pws)
+                                                  + 12 * num_buckets(st["n"], args.bucket) for st in state),
+                  "K2_quantize_stochastic_philox": sum(4 * st["g"].numel + codes_bytes(st["g"].numel, pgs)
+                                                       + 12 * num_buckets(st["g"].numel, args.bucket) for st in state)}
+        philox = {"noise": "np.random.Generator(np.random.Philox(SeedSequence(key))): Philox4x64-10, counter-based "
+                           "(one 10-round block per 4 draws); K1 on the TMA32 path (one draw per bucket), K2 on the "
+                           "team kernels with the counter-based Coder"}
+        for name, fn in (("K1_quantize_shift_philox", pq_w), ("K2_quantize_stochastic_philox", pq_g)):
+            fn()
+            gk = capture(fn)
+            gk.replay()
+            torch.cuda.synchronize(dev)
+            evk = time_graph(gk, args.steps)
+            torch.cuda.synchronize(dev)
+            tk = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+            philox[name] = {"ms_per_pass": round(tk, 4), "gbs": round(pbytes[name] / (tk * 1e-3) / 1e9, 1),
+                            "frac_of_hbm_peak": round(pbytes[name] / (tk * 1e-3) / 1e9 / hbm_peak, 4),
+                            "bytes_per_pass": pbytes[name], "launches_per_pass": len(state)}
+
     # ---- GPU wire codec over the step's weight messages (world 1) ----
     wire = None
     if world == 1 and not args.no_levels:
@@ -882,7 +915,7 @@ def main():
                              + f"; {K} collectives of each kind in flight (FSDP2 prefetch depth; streams + "
                                "communicators per kind), RS(i) after AG_bwd(i)"}),
             "roofline": roofline, "kernels": kernels, "kernels_unfused": kernels_unfused if world == 1 else None, "cpu_baseline": cpu, "e2e": e2e, "gpt": gpt,
-            "levels": levels, "wire": wire, "lattice": lattice,
+            "levels": levels, "philox": philox, "wire": wire, "lattice": lattice,
             "gpu_launches": n_launch * args.steps, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -71,7 +71,15 @@ typedef enum {
 } qsdp_status;
 
 typedef enum { QSDP_INNER_SHIFT = 0, QSDP_INNER_STOCHASTIC = 1, QSDP_INNER_LEVELS = 2 } qsdp_inner;
-typedef enum { QSDP_NOISE_PCG64_SEEDSEQ = 0 } qsdp_noise;
+/* Noise of the quantizers' draws, keyed per bucket by (root, step, layer, phase, worker,
+ * start) through numpy's SeedSequence:
+ *   QSDP_NOISE_PCG64_SEEDSEQ  np.random.default_rng(SeedSequence(key)) == bucket_rng
+ *                             (sharded.py:235-240): sequential 128-bit LCG stream;
+ *   QSDP_NOISE_PHILOX4x64     np.random.Generator(np.random.Philox(SeedSequence(key))):
+ *                             counter-based Philox4x64-10 (key = generate_state(2, uint64)),
+ *                             draw i = word i%4 of block i/4 + 1 -- any generator the
+ *                             reference's quantize_bucket accepts (quantize.py:235-241). */
+typedef enum { QSDP_NOISE_PCG64_SEEDSEQ = 0, QSDP_NOISE_PHILOX4x64 = 1 } qsdp_noise;
 typedef enum { QSDP_F32 = 0, QSDP_F64 = 1, QSDP_BF16 = 2 } qsdp_dtype;
 
 /* mirrors QuantConfig (sharded.py:76-93) for one tensor class */

@@ -71,6 +71,13 @@ def lib():
         L.qo_quantize_segment.argtypes = qargs
         L.qo_quantize_segment.restype = i64
         L.qo_quantize_segment_f32.argtypes = qargs
+        L.qo_quantize_segment_nz.argtypes = qargs + [i32]
+        L.qo_quantize_segment_nz.restype = i64
+        L.qo_quantize_segment_f32_nz.argtypes = qargs + [i32]
+        L.qo_quantize_segment_f32_nz.restype = i64
+        L.qo_philox_rng.argtypes = [vp, u64, u64, u64, u64, u64, u64]
+        L.qo_philox_next.argtypes = [vp]
+        L.qo_philox_next.restype = u64
         L.qo_quantize_segment_f32.restype = i64
         L.qo_dequantize_segment.argtypes = [vp, vp, i64, i64, i32, vp, i32]
         L.qo_dequantize_segment.restype = i32
@@ -118,6 +125,23 @@ class PCG64:
         return float(lib().qo_next_double(_ptr(self._st)))
 
 
+class Philox:
+    """Restated numpy Philox4x64-10 stream: Generator(Philox(SeedSequence(key6)))."""
+
+    def __init__(self, root, step, layer, phase, worker, start):
+        self._st = np.zeros(16, dtype=np.uint64)  # qo_philox: ctr[4], key[2], buf[4], pos
+        lib().qo_philox_rng(_ptr(self._st), root, step, layer, phase, worker, start)
+
+    def next_raw(self) -> int:
+        return int(lib().qo_philox_next(_ptr(self._st)))
+
+    def random(self) -> float:
+        return (self.next_raw() >> 11) * 2.0 ** -53
+
+
+NOISE = {"pcg64": 0, "philox": 1}
+
+
 # -- per-bucket / per-segment quantizer -------------------------------------------
 
 
@@ -133,22 +157,23 @@ def message_size_bits(length: int, bucket: int, bits: int) -> int:
     return int(lib().qo_message_size_bits(length, bucket, bits))
 
 
-def quantize_segment(x, global_start, bucket, bits, inner, key, nthreads=1):
+def quantize_segment(x, global_start, bucket, bits, inner, key, nthreads=1, noise=0):
     """Returns (packed codes uint8, meta float32[nb,3] = shift, lo, hi, bad_index).
 
     ``key`` = (root_seed, step, layer, phase, worker); bucket j is keyed with
-    start = global_start + j*bucket (sharded.py:243-248).
+    start = global_start + j*bucket (sharded.py:243-248).  ``noise`` 0: PCG64
+    (bucket_rng), 1: Philox4x64-10 with the same SeedSequence key.
     """
     x = np.ascontiguousarray(x)
     n = x.size
     codes = np.zeros(max(codes_bytes(n, bucket, bits), 1), dtype=np.uint8)
     meta = np.zeros((max(num_buckets(n, bucket), 1), 3), dtype=np.float32)
-    fn = lib().qo_quantize_segment_f32 if x.dtype == np.float32 else lib().qo_quantize_segment
+    fn = lib().qo_quantize_segment_f32_nz if x.dtype == np.float32 else lib().qo_quantize_segment_nz
     if x.dtype != np.float32:
         x = np.ascontiguousarray(x, dtype=np.float64)
     root, step, layer, phase, worker = key
     bad = fn(_ptr(x), n, global_start, bucket, bits, inner, root, step, layer, phase, worker,
-             _ptr(codes), _ptr(meta), nthreads)
+             _ptr(codes), _ptr(meta), nthreads, int(noise))
     return codes[: codes_bytes(n, bucket, bits)], meta[: num_buckets(n, bucket)], int(bad)
 
 

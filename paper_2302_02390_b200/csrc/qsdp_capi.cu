@@ -31,6 +31,7 @@
 namespace qsdp {
 cudaError_t launch_quantize_f32(const QJobTable& tab, bool vec, int sms, cudaStream_t s);
 cudaError_t launch_quantize_f64(const QJobTable& tab, bool vec, int sms, cudaStream_t s);
+cudaError_t launch_quantize_philox(const QJobTable& tab, bool f64, bool vec, int sms, cudaStream_t s);
 cudaError_t launch_dequant(const DJobTable& tab, bool vec, int sms, cudaStream_t s);
 cudaError_t upload_jump_f32(const JumpEntry* host);
 cudaError_t upload_jump_f64(const JumpEntry* host);
@@ -111,7 +112,8 @@ qsdp_status check_cfg(const qsdp_qcfg* c, bool levels = false) {
   if (c->bucket < 1) return fail(QSDP_EINVAL, "bucket_size must be >= 1");
   if (levels ? c->inner != QSDP_INNER_LEVELS : (c->inner != QSDP_INNER_SHIFT && c->inner != QSDP_INNER_STOCHASTIC))
     return fail(QSDP_EINVAL, levels ? "levels entry points take inner = QSDP_INNER_LEVELS" : "unknown inner mode");
-  if (c->noise != QSDP_NOISE_PCG64_SEEDSEQ) return fail(QSDP_EINVAL, "unsupported noise mode");
+  if (c->noise != QSDP_NOISE_PCG64_SEEDSEQ && c->noise != QSDP_NOISE_PHILOX4x64)
+    return fail(QSDP_EINVAL, "unsupported noise mode");
   return QSDP_OK;
 }
 
@@ -151,6 +153,7 @@ void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, co
   tab.bits = cfg->bits;
   tab.bucket = cfg->bucket;
   tab.inner = cfg->inner;
+  tab.noise = cfg->noise;
   tab.bad_index = reinterpret_cast<unsigned long long*>(d_bad);
   tab.step_ptr = dyn.step_ptr;
   tab.parity_ptr = dyn.parity_ptr;
@@ -201,6 +204,8 @@ qsdp_status run_quantize(const std::vector<QJobSpec>& jobs, int x_dtype, const q
     bool codes_ok = true;  // wide code stores of the levels fast path
     for (int k = 0; k < tab.njobs; ++k) codes_ok = codes_ok && aligned(tab.jobs[k].codes, 8);
     cudaError_t e = levels != nullptr      ? launch_quantize_levels(tab, x_dtype == QSDP_F64, levels, nlevels, vec && codes_ok, sms, stream)
+                    : cfg->noise == QSDP_NOISE_PHILOX4x64 && cfg->inner == QSDP_INNER_STOCHASTIC
+                          ? launch_quantize_philox(tab, x_dtype == QSDP_F64, vec, sms, stream)
                     : x_dtype == QSDP_F64 ? launch_quantize_f64(tab, vec, sms, stream)
                                           : launch_quantize_f32(tab, vec, sms, stream);
     if (e != cudaSuccess) return cuda_fail(e, "quantize kernel launch");
@@ -985,8 +990,9 @@ static QJobSpec comm_qjob(const void* x, const qsdp_segment& seg, uint8_t* slot,
 static bool push_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
   const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
   const int isz = in_dtype == QSDP_F64 ? 8 : 4;
-  return c->world > 1 && cfg->inner != QSDP_INNER_LEVELS && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 72 &&
-         cfg->bucket * isz <= 8192;
+  return c->world > 1 && cfg->inner != QSDP_INNER_LEVELS &&
+         (cfg->noise == QSDP_NOISE_PCG64_SEEDSEQ || cfg->inner == QSDP_INNER_SHIFT) && direct &&
+         cfg->bucket % 8 == 0 && cfg->bucket >= 72 && cfg->bucket * isz <= 8192;
 }
 
 // The fused dequant epilogue lives in the TMA32 quantizer: direct widths,
@@ -997,8 +1003,10 @@ static bool fdq_ok(const qsdp_qcfg* cfg, int in_dtype, int out_dtype) {
   if (off) return false;
   const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
   const int isz = in_dtype == QSDP_F64 ? 8 : 4;
-  return cfg->inner != QSDP_INNER_LEVELS && direct && cfg->bucket % 8 == 0 && cfg->bucket >= 72 &&
-         cfg->bucket * isz <= 8192 && (out_dtype == QSDP_F32 || out_dtype == QSDP_F64 || out_dtype == QSDP_BF16);
+  return cfg->inner != QSDP_INNER_LEVELS &&
+         (cfg->noise == QSDP_NOISE_PCG64_SEEDSEQ || cfg->inner == QSDP_INNER_SHIFT) && direct && cfg->bucket % 8 == 0 &&
+         cfg->bucket >= 72 && cfg->bucket * isz <= 8192 &&
+         (out_dtype == QSDP_F32 || out_dtype == QSDP_F64 || out_dtype == QSDP_BF16);
 }
 
 qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, const qsdp_segment* segs,

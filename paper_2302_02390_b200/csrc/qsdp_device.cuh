@@ -149,6 +149,63 @@ __host__ __device__ __forceinline__ SeedPrefix make_prefix(uint64_t root, uint64
   return p;
 }
 
+// ---------------------------------------------------------------------------
+// Counter-based noise: numpy's Philox (Philox4x64-10, numpy/random/src/philox),
+// the generator np.random.Generator(np.random.Philox(SeedSequence(key6))).  Its
+// key is SeedSequence.generate_state(2, uint64) -- the first four words of the same
+// pool the PCG64 seeding draws -- and draw i is word i % 4 of the block with
+// counter i / 4 + 1 (numpy increments the counter before its first block), so any
+// element's draw is computed directly: no sequential state.
+// ---------------------------------------------------------------------------
+constexpr uint64_t PHILOX_M0 = 0xD2E7470EE14C6C93ull, PHILOX_M1 = 0xCA5A826395121157ull;
+constexpr uint64_t PHILOX_W0 = 0x9E3779B97F4A7C15ull, PHILOX_W1 = 0xBB67AE8584CAA73Bull;
+struct Philox4 {
+  uint64_t v[4];
+};
+__host__ __device__ __forceinline__ Philox4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
+                                                          uint64_t k0, uint64_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += PHILOX_W0;
+      k1 += PHILOX_W1;
+    }
+    const uint64_t lo0 = PHILOX_M0 * c0, hi0 = mulhi64(PHILOX_M0, c0);
+    const uint64_t lo1 = PHILOX_M1 * c2, hi1 = mulhi64(PHILOX_M1, c2);
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return Philox4{{c0, c1, c2, c3}};
+}
+// Block `blk` (0-based) of a fresh numpy Philox: counter blk + 1 (256-bit, carry into word 1).
+__host__ __device__ __forceinline__ Philox4 philox_block(uint64_t blk, uint64_t k0, uint64_t k1) {
+  const uint64_t c0 = blk + 1ull;
+  return philox4x64_10(c0, c0 == 0 ? 1ull : 0ull, 0, 0, k0, k1);
+}
+// SeedSequence(prefix + start).generate_state(2, uint64) -> (k0, k1)
+__host__ __device__ __forceinline__ void philox_key(const SeedPrefix& pre, uint64_t start, uint64_t& k0,
+                                                    uint64_t& k1) {
+  uint32_t pool[4] = {pre.pool[0], pre.pool[1], pre.pool[2], pre.pool[3]};
+  uint32_t hc = pre.hash_const;
+  ss_absorb_u64(pool, hc, start);
+  uint32_t st[4];
+  uint32_t hb = SS_INIT_B;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t v = pool[i];
+    v ^= hb;
+    hb *= SS_MULT_B;
+    v *= hb;
+    v ^= v >> 16;
+    st[i] = v;
+  }
+  k0 = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
+  k1 = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+}
+
 // One PCG64 step (state <- state*M + inc) and XSL-RR output of the new state.
 __host__ __device__ __forceinline__ uint64_t pcg_output(U128 s) {
   const uint64_t x = s.hi ^ s.lo;
@@ -224,7 +281,7 @@ struct QJobTable {
   int32_t dq_dtype;
   int32_t dq_add0;
   int32_t dq_nocodes;  // world 1: the fused dequant is the only consumer -> codes not stored
-  int32_t _pad_dq;
+  int32_t noise;       // qsdp_noise: 0 PCG64 (bucket_rng), 1 Philox4x64-10 (counter-based)
 };
 
 struct DJob {

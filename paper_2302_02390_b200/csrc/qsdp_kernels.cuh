@@ -201,6 +201,18 @@ static __device__ __noinline__ uint32_t exact_stoch_code(double a, double span, 
   return (uint32_t)c;
 }
 
+static __device__ __noinline__ uint32_t exact_stoch_code_d(double a, double span, double top, uint64_t draw) {
+  double u = __ddiv_rn(a, span);
+  u = fmin(fmax(u, 0.0), 1.0);
+  const double s = __dmul_rn(u, top);
+  const double low = floor(s);
+  const double frac = __dsub_rn(s, low);
+  const double d = u64_to_unit_double(draw);
+  double c = low + (d < frac ? 1.0 : 0.0);
+  c = fmin(fmax(c, 0.0), top);
+  return (uint32_t)c;
+}
+
 template <int TL, typename K>
 __device__ __forceinline__ K team_min_k(K v) {
 #pragma unroll
@@ -249,20 +261,35 @@ __host__ __device__ __forceinline__ bool direct_width(int bits) {
 // ---------------------------------------------------------------------------
 // Per-bucket quantization context and the per-element certified fast path.
 // ---------------------------------------------------------------------------
-template <typename T, int INNER>
+// NZ: the noise source -- 0 numpy PCG64 (bucket_rng, sequential stream with jumps),
+// 1 numpy Philox4x64-10 (counter-based: st holds the key, a group's 4 draws are one block).
+template <typename T, int INNER, int NZ = 0>
 struct Coder {
   double lo, span, inv, pitch, top, r;
   U128 st, inc, jmp_a, jmp_c;
 
   // Bucket setup: scales, noise.  `lt` = lane in team, TL = team lanes.
+  // noise: the table's qsdp_noise at run time -- Philox shift buckets (one draw) share the
+  // PCG64 kernels; Philox stochastic buckets run the NZ == 1 instantiations.
   __device__ __forceinline__ void setup(float lof, float hif, int bits, const SeedPrefix& seed, uint64_t start,
-                                        int lt, int TL, float& shift_f) {
+                                        int lt, int TL, float& shift_f, int noise = 0) {
     top = (double)((1u << bits) - 1u);
     lo = (double)lof;
     span = __dsub_rn((double)hif, lo);
     inv = __drcp_rn(span);
     pitch = __ddiv_rn(1.0, top);
     r = 0.0;
+    if (NZ == 1 || (INNER == 0 && noise == 1)) {
+      philox_key(seed, start, st.lo, st.hi);
+      if (INNER == 0) {  // sample_shift's single draw: word 0 of block 0
+        const double d = u64_to_unit_double(philox_block(0, st.lo, st.hi).v[0]);
+        r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));
+        shift_f = __double2float_rn(__dmul_rn(r, span));
+      } else {
+        shift_f = 0.0f;
+      }
+      return;
+    }
     seed_bucket(seed, start, st, inc);
     if (INNER == 0) {
       // sample_shift(pitch): uniform(-p/2, p/2) = -p/2 + p*d, unfused (quantize.py:130-132)
@@ -279,6 +306,20 @@ struct Coder {
       jmp_c = mul128(ej.g, inc);
       shift_f = 0.0f;
     }
+  }
+
+  // Stochastic code of one element given its raw 64-bit draw (certified, exact fallback).
+  __device__ __forceinline__ uint32_t code_draw(T t, uint64_t draw) {
+    const double a = __dsub_rn(InTraits<T>::to_d(t), lo);
+    const bool at_hi = a >= span;
+    const bool at_lo = a <= 0.0;
+    const double u = at_hi ? 1.0 : (at_lo ? 0.0 : __dmul_rn(a, inv));
+    const Fixed32 q = fixed32(__dmul_rn(u, top));
+    const uint32_t dh = (uint32_t)(draw >> 32);
+    if (at_hi || at_lo) return (uint32_t)q.ip;
+    if (q.frac - dh <= 1u) return exact_stoch_code_d(a, span, top, draw);
+    const int c = q.ip + (q.frac > dh ? 1 : 0);
+    return (uint32_t)min(c, (int)top);
   }
 
   // Code of one element; for INNER 1 uses the current state (caller steps it).
@@ -312,6 +353,16 @@ struct Coder {
   // 4 codes of group starting at element e (elements >= n coded 0), packed LSB-first.
   __device__ __forceinline__ uint64_t group(const T v[4], int e, int n, int bits) {
     uint64_t w = 0;
+    if constexpr (NZ == 1 && INNER == 1) {  // elements e..e+3 draw words 0..3 of block e / 4
+      const Philox4 d = philox_block((uint64_t)(e >> 2), st.lo, st.hi);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t c = code_draw(v[i], d.v[i]);
+        c = (e + i < n) ? c : 0u;
+        w |= (uint64_t)c << (i * bits);
+      }
+      return w;
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       uint32_t c = code(v[i]);
@@ -514,7 +565,8 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
     // ---- pass 2: codes ----------------------------------------------------------
     Coder<T, INNER> cd;
     float shift_f = 0.0f;
-    if (active && !degenerate) cd.setup(lof, hif, BITS, q_seed(tab, J), (uint64_t)(J.global_start + br.off), lt, TL, shift_f);
+    if (active && !degenerate)
+      cd.setup(lof, hif, BITS, q_seed(tab, J), (uint64_t)(J.global_start + br.off), lt, TL, shift_f, tab.noise);
     uint8_t* cbase = J.codes + poff + br.lb * pbs;
     const int64_t pb = payload_bytes(n, BITS);
     if (active && !degenerate && in_smem) {
@@ -679,7 +731,7 @@ static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix
                                                              const QJob& J, int64_t off) {
   Coder<T, INNER> cd;
   float shift_f = 0.0f;
-  if (!degenerate) cd.setup(lof, hif, BITS, seed, start, lane, 32, shift_f);
+  if (!degenerate) cd.setup(lof, hif, BITS, seed, start, lane, 32, shift_f, tab.noise);
   const FusedDq fq = fused_dq<FDQ>(tab, J, off, lof, hif, degenerate ? 0.0f : shift_f, BITS);
   const int64_t pb = payload_bytes(n, BITS);
   for (int g = 0; g < gl; ++g) {
@@ -766,6 +818,13 @@ __device__ __forceinline__ SeedOut seed_for(const QJobTable& tab, int64_t b, int
   if (b < tab.total_buckets) {
     const BucketRef br = resolve_q(tab, b, S);
     const QJob& J = tab.jobs[br.j];
+    if (INNER == 0 && tab.noise == 1) {  // Philox: sample_shift's draw = word 0 of block 0
+      uint64_t k0, k1;
+      philox_key(q_seed(tab, J), (uint64_t)(J.global_start + br.off), k0, k1);
+      const double d = u64_to_unit_double(philox_block(0, k0, k1).v[0]);
+      o.r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));
+      return o;
+    }
     seed_bucket(q_seed(tab, J), (uint64_t)(J.global_start + br.off), o.s0, o.inc);
     if (INNER == 0) {
       const U128 s1 = mad128(o.s0, pcg_mult(), o.inc);
@@ -1173,7 +1232,7 @@ __device__ __forceinline__ void store_pair(uint8_t* cbase, int gi, uint64_t w, u
   }
 }
 
-template <typename T, int INNER, int TL, int G, bool HOLD, bool VEC>
+template <typename T, int INNER, int TL, int G, bool HOLD, bool VEC, int NZ = 0>
 __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ QJobTable tab) {
   const int64_t poff = q_parity_off(tab);
   constexpr int TEAMS = 32 / TL;
@@ -1241,9 +1300,10 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
       atomicMin(tab.bad_index, ((unsigned long long)br.j << 40) | (unsigned long long)(br.off + i));
     }
 
-    Coder<T, INNER> cd;
+    Coder<T, INNER, NZ> cd;
     float shift_f = 0.0f;
-    if (active && !degenerate) cd.setup(lof, hif, bits, q_seed(tab, J), (uint64_t)(J.global_start + br.off), lt, TL, shift_f);
+    if (active && !degenerate)
+      cd.setup(lof, hif, bits, q_seed(tab, J), (uint64_t)(J.global_start + br.off), lt, TL, shift_f, tab.noise);
     uint8_t* cbase = J.codes + poff + br.lb * pbs;
     const int64_t pb = payload_bytes(n, bits);
     auto emit = [&](const T t[4], int g) {
@@ -1290,7 +1350,7 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
 // Generic quantizer for bucket sizes that are not a multiple of 8: one thread
 // per bucket, exact fp64 chain for every element, bit-serial packing.
 // ---------------------------------------------------------------------------
-template <typename T, int INNER>
+template <typename T, int INNER, int NZ = 0>
 __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_constant__ QJobTable tab) {
   const int64_t poff = q_parity_off(tab);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1324,10 +1384,12 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
     double r = 0.0;
     float shift_f = 0.0f;
     if (!degenerate) {
-      seed_bucket(q_seed(tab, J), (uint64_t)(J.global_start + br.off), st, inc);
+      const bool ph = NZ == 1 || tab.noise == 1;
+      if (ph) philox_key(q_seed(tab, J), (uint64_t)(J.global_start + br.off), st.lo, st.hi);
+      else seed_bucket(q_seed(tab, J), (uint64_t)(J.global_start + br.off), st, inc);
       if (INNER == 0) {
-        st = pcg_step(st, inc);
-        const double d = u64_to_unit_double(pcg_output(st));
+        if (!ph) st = pcg_step(st, inc);
+        const double d = u64_to_unit_double(ph ? philox_block(0, st.lo, st.hi).v[0] : pcg_output(st));
         r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));
         shift_f = __double2float_rn(__dmul_rn(r, span));
       }
@@ -1341,6 +1403,8 @@ __global__ void __launch_bounds__(128) quantize_generic_kernel(const __grid_cons
         const double a = __dsub_rn(Tr::to_d(x[i]), lo);
         if (INNER == 0) {
           code = exact_shift_code(a, span, r, pitch, top);
+        } else if (NZ == 1) {
+          code = exact_stoch_code_d(a, span, top, philox_block((uint64_t)(i >> 2), st.lo, st.hi).v[i & 3]);
         } else {
           st = pcg_step(st, inc);
           code = exact_stoch_code(a, span, top, st);
@@ -2041,6 +2105,44 @@ cudaError_t launch_q_tl(const QJobTable& tab, bool vec, int sms, cudaStream_t s)
     else go(quantize_kernel<T, INNER, TL, 1, false, false>);
   }
   return cudaGetLastError();
+}
+
+// Philox noise (qsdp_noise 1): the team kernels with the counter-based Coder (any width,
+// S % 8 == 0), or the generic kernel; the TMA fast paths are PCG64-only.
+template <typename T, int INNER, int TL>
+cudaError_t launch_q_philox_tl(const QJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  const int S = tab.bucket;
+  constexpr int G = TL == 32 ? 8 : 1;
+  const int gl = ((S + 3) / 4 + TL - 1) / TL;
+  auto go = [&](auto kern) {
+    kern<<<persistent_grid(kern, 256, 0, tab.total_buckets, 32 / TL, sms), 256, 0, s>>>(tab);
+  };
+  if (TL < 32 || gl <= G) {
+    if (vec) go(quantize_kernel<T, INNER, TL, G, true, true, 1>);
+    else go(quantize_kernel<T, INNER, TL, G, true, false, 1>);
+  } else if constexpr (TL == 32) {
+    if (vec) go(quantize_kernel<T, INNER, TL, 1, false, true, 1>);
+    else go(quantize_kernel<T, INNER, TL, 1, false, false, 1>);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T, int INNER>
+cudaError_t launch_q_philox(const QJobTable& tab, bool vec, int sms, cudaStream_t s) {
+  const int S = tab.bucket;
+  if (S % 8 != 0) {
+    const int64_t blocks = (tab.total_buckets + 127) / 128;
+    const int64_t cap = (int64_t)sms * 16;
+    quantize_generic_kernel<T, INNER, 1><<<(int)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks)), 128, 0, s>>>(tab);
+    return cudaGetLastError();
+  }
+  switch (team_lanes(S)) {
+    case 2: return launch_q_philox_tl<T, INNER, 2>(tab, vec, sms, s);
+    case 4: return launch_q_philox_tl<T, INNER, 4>(tab, vec, sms, s);
+    case 8: return launch_q_philox_tl<T, INNER, 8>(tab, vec, sms, s);
+    case 16: return launch_q_philox_tl<T, INNER, 16>(tab, vec, sms, s);
+    default: return launch_q_philox_tl<T, INNER, 32>(tab, vec, sms, s);
+  }
 }
 
 template <typename T, int INNER>

@@ -29,7 +29,8 @@ import torch
 from . import _lib
 
 __all__ = [
-    "QuantSpec", "SegmentKey", "BucketSpec", "QuantizedBlock", "KeyedBucketRNG", "bucket_rng",
+    "QuantSpec", "SegmentKey", "BucketSpec", "QuantizedBlock", "KeyedBucketRNG", "bucket_rng", "philox_rng",
+    "NOISE_MODES",
     "num_buckets", "codes_bytes", "message_size_bits", "quantize_segments", "quantize_segment",
     "dequantize_segments", "dequantize_segment", "dequant_accumulate", "quantize_bucket",
     "bucketed_quantize", "dequantize", "INNER_MODES", "advance_counter",
@@ -40,6 +41,9 @@ INNER_MODES = AFFINE_MODES + ("levels",)
 _INNER_CODE = {"shift": _lib.INNER_SHIFT, "flip": _lib.INNER_STOCHASTIC,
                "uniform_stochastic": _lib.INNER_STOCHASTIC, "levels": _lib.INNER_LEVELS}
 _DTYPE_CODE = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16}
+# the quantizers' noise (qsdp_noise): "pcg64" = bucket_rng's default_rng(SeedSequence(key)),
+# "philox" = Generator(Philox(SeedSequence(key))) -- counter-based, same keys
+NOISE_MODES = {"pcg64": 0, "philox": 1}
 
 
 @dataclass(frozen=True)
@@ -49,6 +53,7 @@ class QuantSpec:
     bits: int = 8
     bucket: int = 1024
     inner: str = "shift"
+    noise: str = "pcg64"
 
     def __post_init__(self):
         if not 1 <= self.bits <= 16:
@@ -57,9 +62,11 @@ class QuantSpec:
             raise ValueError(f"bucket_size must be >= 1, got {self.bucket}")
         if self.inner not in _INNER_CODE:
             raise ValueError(f"unknown inner mode {self.inner!r}")
+        if self.noise not in NOISE_MODES:
+            raise ValueError(f"unknown noise mode {self.noise!r}")
 
     def cfg(self) -> _lib.QCfg:
-        return _lib.QCfg(self.bits, self.bucket, _INNER_CODE[self.inner], 0)
+        return _lib.QCfg(self.bits, self.bucket, _INNER_CODE[self.inner], NOISE_MODES[self.noise])
 
 
 @dataclass(frozen=True)
@@ -287,13 +294,15 @@ class QuantizedBlock:
 
 class KeyedBucketRNG:
     """What ``bucket_rng`` returns here: the key of one quantization event.
-    The device regenerates numpy's SeedSequence(key) -> PCG64 stream from it."""
+    The device regenerates numpy's SeedSequence(key) -> PCG64 stream from it
+    (``noise="philox"``: the Philox4x64-10 stream of the same SeedSequence)."""
 
-    __slots__ = ("key", "start")
+    __slots__ = ("key", "start", "noise")
 
-    def __init__(self, root_seed, step, layer_idx, phase, worker, start):
+    def __init__(self, root_seed, step, layer_idx, phase, worker, start, noise="pcg64"):
         self.key = SegmentKey(int(root_seed), int(step), int(layer_idx), int(phase), int(worker))
         self.start = int(start)
+        self.noise = noise
 
 
 def bucket_rng(root_seed: int, step: int, layer_idx: int, phase: int, worker: int,
@@ -303,6 +312,17 @@ def bucket_rng(root_seed: int, step: int, layer_idx: int, phase: int, worker: in
         if int(v) < 0:
             raise ValueError("expected non-negative integer key fields")
     return KeyedBucketRNG(root_seed, step, layer_idx, phase, worker, start)
+
+
+def philox_rng(root_seed: int, step: int, layer_idx: int, phase: int, worker: int,
+               start: int) -> KeyedBucketRNG:
+    """The counter-based generator of the same key:
+    ``np.random.Generator(np.random.Philox(SeedSequence((root, step, layer, phase, worker, start))))``
+    -- a generator the reference's ``quantize_bucket`` accepts (quantize.py:235-241)."""
+    for v in (root_seed, step, layer_idx, phase, worker, start):
+        if int(v) < 0:
+            raise ValueError("expected non-negative integer key fields")
+    return KeyedBucketRNG(root_seed, step, layer_idx, phase, worker, start, noise="philox")
 
 
 def _unpack(packed: np.ndarray, n: int, bits: int) -> np.ndarray:
@@ -345,7 +365,7 @@ def quantize_bucket(values, bit_width: int, inner: str, rng: KeyedBucketRNG, lev
         return _levels_blocks(v, v.size, bit_width, levels)[0]
     if not isinstance(rng, KeyedBucketRNG):
         raise TypeError("rng must come from bucket_rng(...): the device reproduces keyed streams")
-    spec = QuantSpec(bit_width, v.size, inner)
+    spec = QuantSpec(bit_width, v.size, inner, rng.noise)
     x = torch.from_numpy(np.ascontiguousarray(v)).to(_device())
     codes, meta = quantize_segment(x, rng.start, spec, rng.key, check_finite=True)
     return _blocks_from_device(codes, meta, v.size, v.size, bit_width)[0]
@@ -368,7 +388,7 @@ def bucketed_quantize(v, bucket: BucketSpec, bit_width: int, inner: str = "shift
         return _levels_blocks(v, bucket.bucket_size, bit_width, levels)
     if not isinstance(rng, KeyedBucketRNG):
         raise TypeError("rng must come from bucket_rng(...)")
-    spec = QuantSpec(bit_width, bucket.bucket_size, inner)
+    spec = QuantSpec(bit_width, bucket.bucket_size, inner, rng.noise)
     x = torch.from_numpy(np.ascontiguousarray(v)).to(_device())
     codes, meta = quantize_segment(x, rng.start, spec, rng.key, check_finite=True)
     return _blocks_from_device(codes, meta, v.size, bucket.bucket_size, bit_width)

@@ -10,6 +10,7 @@ if ROOT not in sys.path:
 
 REFERENCE_SRC = "/root/reference/pkg/src"
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.npz")
+GOLDEN_PHILOX = os.path.join(ROOT, "tests", "golden", "golden_philox.npz")
 
 
 def pytest_configure(config):
@@ -36,6 +37,19 @@ def pytest_collection_modifyitems(config, items):
 @pytest.fixture(scope="session")
 def golden():
     return np.load(GOLDEN, allow_pickle=False)
+
+
+@pytest.fixture(scope="session")
+def golden_philox():
+    return np.load(GOLDEN_PHILOX, allow_pickle=False)
+
+
+def golden_philox_cases(g):
+    """The quantizer cases of golden_philox.npz (reference quantize_bucket + numpy Philox)."""
+    for i, r in enumerate(g["phq_cases"]):
+        bits, inner, S, n, start, root, step, layer, phase, worker = (int(v) for v in r)
+        yield dict(i=i, bits=bits, inner=inner, bucket=S, n=n, start=start, key=(root, step, layer, phase, worker),
+                   x=g[f"phq_{i}_x"], codes=g[f"phq_{i}_codes"], meta=g[f"phq_{i}_meta"], deq=g[f"phq_{i}_deq"])
 
 
 @pytest.fixture(scope="session")

@@ -110,6 +110,7 @@ def main():
                 print(f"rank {rank} size {size} graph replay {rep}: mismatch", flush=True)
         comm.close()
     failures += offset_views(rank, world, dev)
+    failures += philox_collectives(rank, world, dev)
     failures += levels_all_gather(rank, world, dev)
     failures += lattice_reduce_scatter(rank, world, dev)
     failures += pipelined(rank, world, dev)
@@ -270,6 +271,37 @@ def missed_barrier(rank, world, dev):
         except QSDPError:
             pass
     dist.barrier()
+    comm.close()
+    return fails
+
+
+def philox_collectives(rank, world, dev):
+    """C1/C2 with the counter-based noise (QSDP_NOISE_PHILOX4x64) at world > 1 (pull form)."""
+    fails = 0
+    size, bucket = 500009, 1024
+    segs = plan_segments(size, world, 1)
+    ws, gs = QuantSpec(8, bucket, "shift", "philox"), QuantSpec(4, bucket, "uniform_stochastic", "philox")
+    comm = QSDPComm(max(n for _, n in segs), ws, gs)
+    full = (np.random.default_rng(17).standard_normal(size) * 0.02).astype(np.float32)
+    grads = [(np.random.default_rng(170 + p).standard_normal(size) * 1e-3).astype(np.float32) for p in range(world)]
+    s, n = segs[rank]
+    for step in range(2):
+        out = torch.empty(size, device=dev)
+        comm.all_gather(torch.from_numpy(full[s:s + n]).to(dev), segs, SegmentKey(5, step, 1, 0, 0), out)
+        exp = np.zeros(size)
+        for sq, nq in segs:
+            c, m, _ = O.quantize_segment(full[sq:sq + nq], sq, bucket, 8, 0, (5, step, 1, 0, 0), 8, noise=1)
+            exp[sq:sq + nq] = O.dequantize_segment(c, m, nq, bucket, 8, 8)
+        sh = torch.empty(max(n, 1), device=dev)
+        comm.reduce_scatter(torch.from_numpy(grads[rank]).to(dev), segs, SegmentKey(5, step, 1, 2, rank), sh)
+        acc = np.zeros(n)
+        for p in range(world):
+            c, m, _ = O.quantize_segment(grads[p][s:s + n], s, bucket, 4, 1, (5, step, 1, 2, p), 8, noise=1)
+            acc = acc + O.dequantize_segment(c, m, n, bucket, 4, 8)
+        if not (np.array_equal(out.cpu().numpy(), exp.astype(np.float32))
+                and np.array_equal(sh[:n].cpu().numpy(), (acc / world).astype(np.float32))):
+            fails += 1
+            print(f"rank {rank} philox step {step}: mismatch", flush=True)
     comm.close()
     return fails
 

@@ -200,3 +200,43 @@ def test_levels_live_reference_random(oracle, reference):
         blocks = bucketed_quantize(x, BucketSpec(S), bits, "levels", levels=table)
         codes, meta, _ = oracle.quantize_levels_segment(x, S, bits, table.levels)
         assert codes.tobytes() == b"".join(_pack_codes(b.codes, bits) for b in blocks)
+
+
+# -- counter-based noise (numpy Philox4x64-10 keyed like bucket_rng) --------------------
+
+
+def test_philox_draws_match_numpy_golden(golden_philox, oracle):
+    for key, draws in zip(golden_philox["ph_keys"], golden_philox["ph_draws"]):
+        g = oracle.Philox(*(int(k) for k in key))
+        assert [g.next_raw() for _ in range(draws.size)] == [int(d) for d in draws]
+
+
+def test_philox_quantizer_golden(golden_philox, oracle):
+    from conftest import golden_philox_cases
+    for c in golden_philox_cases(golden_philox):
+        codes, meta, bad = oracle.quantize_segment(c["x"], c["start"], c["bucket"], c["bits"], c["inner"], c["key"],
+                                                   4, noise=1)
+        assert bad == -1
+        assert np.array_equal(codes, c["codes"]), c["i"]
+        assert np.array_equal(meta, c["meta"]), c["i"]
+        assert np.array_equal(oracle.dequantize_segment(codes, meta, c["n"], c["bucket"], c["bits"]), c["deq"]), c["i"]
+
+
+@pytest.mark.reference
+def test_philox_live_reference_random(oracle, reference):
+    """quantize_bucket(v, b, inner, Generator(Philox(SeedSequence(key)))) (quantize.py:235-241)
+    on random configurations vs the oracle's Philox restatement."""
+    from qsdp.quantize import quantize_bucket
+    rng = np.random.default_rng(77)
+    for t in range(30):
+        bits = int(rng.integers(1, 17))
+        inner = int(rng.integers(0, 2))
+        n = int(rng.integers(1, 700))
+        key = tuple(int(v) for v in rng.integers(0, 2**33, 5))
+        start = int(rng.integers(0, 2**40))
+        v = rng.standard_normal(n) * float(rng.choice([1e-3, 0.02, 3.0]))
+        gen = np.random.Generator(np.random.Philox(np.random.SeedSequence(key + (start,))))
+        blk = quantize_bucket(v, bits, "shift" if inner == 0 else "uniform_stochastic", gen)
+        codes, meta, _ = oracle.quantize_segment(v, start, n, bits, inner, key, 1, noise=1)
+        assert np.array_equal(oracle.unpack(codes, n, bits), blk.codes), t
+        assert (float(meta[0, 0]), float(meta[0, 1]), float(meta[0, 2])) == (blk.shift, blk.scale_lo, blk.scale_hi), t
