@@ -284,6 +284,26 @@ qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_
 qsdp_status qsdp_reduce_scatter_lattice(qsdp_comm* c, const void* full_grad, int32_t in_dtype,
                                         const qsdp_segment* segs, const qsdp_key* key, void* shard_out,
                                         int32_t out_dtype, void* x_shard, const qsdp_lattice* lat, void* stream);
+/* Group collectives: npieces equal-per-rank pieces in one call -- e.g. an FSDP2 group's
+ * dense parameters, piece k at element offset_k of every rank's flat buffer of
+ * rank_stride elements.  Piece k of rank q is keyed with start = q*rank_stride + offset_k;
+ * one quantize launch, one barrier and one dequant launch per call.
+ *   all-gather:     src = this rank's piece (numel elements); full_out[q*rank_stride + offset_k ...]
+ *                   receives rank q's dequantized piece.
+ *   reduce-scatter: src = piece k of destination 0 in this rank's rank-major gradient
+ *                   (destination q's piece at src + q*rank_stride elements); shard_out[offset_k ...]
+ *                   receives the fp64-ordered average over ranks.
+ * The pieces' codes + meta must fit the communicator's slot (max_segment_elems). */
+typedef struct {
+  const void* src;
+  int64_t offset, numel;
+} qsdp_piece;
+qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32_t npieces, int32_t in_dtype,
+                                   int64_t rank_stride, const qsdp_key* key, void* full_out, int32_t out_dtype,
+                                   void* stream);
+qsdp_status qsdp_reduce_scatter_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32_t npieces, int32_t in_dtype,
+                                       int64_t rank_stride, const qsdp_key* key, void* shard_out, int32_t out_dtype,
+                                       void* stream);
 qsdp_status qsdp_comm_destroy(qsdp_comm* c);
 
 #ifdef __cplusplus

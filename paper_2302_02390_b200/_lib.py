@@ -44,8 +44,13 @@ EXPORTED_SYMBOLS = (
     "qsdp_dequantize_levels_batch", "qsdp_learn_levels", "qsdp_comm_set_weight_levels",
     "qsdp_wire_parse", "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes",
     "qsdp_unpack_codes", "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice",
-    "qsdp_comm_set_sm_budget", "qsdp_comm_set_timeout", "qsdp_comm_status",
+    "qsdp_comm_set_sm_budget", "qsdp_comm_set_timeout", "qsdp_comm_status", "qsdp_all_gather_pieces",
+    "qsdp_reduce_scatter_pieces",
 )
+
+
+class Piece(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("offset", ctypes.c_int64), ("numel", ctypes.c_int64)]
 
 
 class QCfg(ctypes.Structure):
@@ -154,6 +159,8 @@ def lib():
     L.qsdp_comm_set_sm_budget.argtypes = [vp, i32]
     L.qsdp_comm_set_timeout.argtypes = [vp, i64]
     L.qsdp_comm_status.argtypes = [vp]
+    L.qsdp_all_gather_pieces.argtypes = [vp, ctypes.POINTER(Piece), i32, i32, i64, keyp, vp, i32, vp]
+    L.qsdp_reduce_scatter_pieces.argtypes = [vp, ctypes.POINTER(Piece), i32, i32, i64, keyp, vp, i32, vp]
     L.qsdp_wire_parse.argtypes = [vp, i64, ctypes.POINTER(WireInfo)]
     L.qsdp_wire_encode_device.argtypes = [vp, vp, i64, cfgp, vp, i64, vp]
     L.qsdp_wire_decode_device.argtypes = [vp, ctypes.POINTER(WireInfo), vp, vp, vp, vp]
@@ -189,7 +196,7 @@ def lib():
                  "qsdp_learn_levels", "qsdp_comm_set_weight_levels", "qsdp_wire_parse",
                  "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes", "qsdp_unpack_codes",
                  "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice", "qsdp_comm_set_sm_budget",
-                 "qsdp_comm_set_timeout", "qsdp_comm_status"):
+                 "qsdp_comm_set_timeout", "qsdp_comm_status", "qsdp_all_gather_pieces", "qsdp_reduce_scatter_pieces"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib

@@ -216,6 +216,41 @@ class QSDPComm:
                 _DTYPE_CODE[out.dtype], torch.cuda.current_stream(self.device).cuda_stream))
         return out
 
+    @staticmethod
+    def _pieces(pieces):
+        arr = (_lib.Piece * len(pieces))()
+        for k, (src, off, n) in enumerate(pieces):
+            arr[k] = _lib.Piece(src.data_ptr() if src is not None else None, int(off), int(n))
+        return arr
+
+    def all_gather_pieces(self, pieces, rank_stride: int, key: SegmentKey, out: torch.Tensor,
+                          in_dtype=torch.float32) -> torch.Tensor:
+        """C1 over a group of pieces in one call: ``pieces`` = [(this rank's piece tensor, offset,
+        numel)]; rank q's piece k lands at ``out[q * rank_stride + offset]`` (keyed start)."""
+        arr = self._pieces(pieces)
+        k = key.c()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().qsdp_all_gather_pieces(
+                self._h, arr, len(pieces), _DTYPE_CODE[in_dtype], int(rank_stride), ctypes.byref(k), out.data_ptr(),
+                _DTYPE_CODE[out.dtype], torch.cuda.current_stream(self.device).cuda_stream))
+        return out
+
+    def reduce_scatter_pieces(self, grad: torch.Tensor, pieces, rank_stride: int, key: SegmentKey,
+                              out: torch.Tensor) -> torch.Tensor:
+        """C2 over a group of pieces: ``grad`` is this rank's rank-major gradient
+        [world * rank_stride]; ``pieces`` = [(offset, numel)]; ``out[offset]`` receives piece k's
+        average."""
+        arr = (_lib.Piece * len(pieces))()
+        esz = grad.element_size()
+        for j, (off, n) in enumerate(pieces):
+            arr[j] = _lib.Piece(grad.data_ptr() + int(off) * esz, int(off), int(n))
+        k = key.c()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().qsdp_reduce_scatter_pieces(
+                self._h, arr, len(pieces), _DTYPE_CODE[grad.dtype], int(rank_stride), ctypes.byref(k), out.data_ptr(),
+                _DTYPE_CODE[out.dtype], torch.cuda.current_stream(self.device).cuda_stream))
+        return out
+
     def reduce_scatter_lattice(self, full_grad: torch.Tensor, segs, key: SegmentKey, x_shard: torch.Tensor,
                                step, out: torch.Tensor | None = None) -> torch.Tensor:
         """C2 + the lattice-projected step on this rank's shard, in the K4 epilogue

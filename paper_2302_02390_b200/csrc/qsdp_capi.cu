@@ -1136,6 +1136,156 @@ static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int3
   return run_dequant(d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 0), nullptr, lat);
 }
 
+// ---------------------------------------------------------------------------
+// Group collectives: several equal-per-rank pieces in one call (an FSDP2 group's
+// dense parameters, each at a fixed offset of every rank's flat buffer).  One
+// quantize launch, one barrier and one dequant launch for the whole group; piece
+// k of rank q is keyed with start = q * rank_stride + offset_k (sharded.py:243-248
+// per piece).  Slot layout: piece k's codes at a 16-byte aligned offset, its meta
+// after all codes -- the same on every rank, derived from the piece list alone.
+// ---------------------------------------------------------------------------
+struct PieceLayout {
+  std::vector<size_t> code_off, meta_off;
+  size_t codes = 0, meta = 0;
+};
+
+static qsdp_status piece_layout(const qsdp_comm* c, const qsdp_qcfg* cfg, const qsdp_piece* pieces, int32_t np,
+                                PieceLayout& L) {
+  if (np < 1 || pieces == nullptr) return fail(QSDP_EINVAL, "need at least one piece");
+  L.code_off.resize(np);
+  L.meta_off.resize(np);
+  for (int k = 0; k < np; ++k) {
+    if (pieces[k].numel < 0 || pieces[k].offset < 0) return fail(QSDP_EINVAL, "negative piece");
+    if (pieces[k].numel > 0 && pieces[k].src == nullptr) return fail(QSDP_EINVAL, "null piece input");
+    L.code_off[k] = L.codes;
+    L.meta_off[k] = L.meta;
+    L.codes += round_up((size_t)qsdp_codes_bytes(pieces[k].numel, cfg), 16);
+    L.meta += (size_t)qsdp_num_buckets(pieces[k].numel, cfg->bucket) * 12;
+  }
+  if (L.codes > c->slot_codes || L.meta > c->slot_meta)
+    return fail(QSDP_EINVAL, "group pieces exceed the communicator's slot (max_segment_elems)");
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32_t npieces, int32_t in_dtype,
+                                   int64_t rank_stride, const qsdp_key* key, void* full_out, int32_t out_dtype,
+                                   void* stream) {
+  if (c == nullptr || key == nullptr || full_out == nullptr) return fail(QSDP_EINVAL, "null argument");
+  qsdp_status st = comm_failed(c);
+  if (st != QSDP_OK) return st;
+  const qsdp_qcfg* cfg = &c->w;
+  if (cfg->inner == QSDP_INNER_LEVELS) return fail(QSDP_EINVAL, "group collectives take affine weight specs");
+  PieceLayout L;
+  st = piece_layout(c, cfg, pieces, npieces, L);
+  if (st != QSDP_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool push = push_ok(c, cfg, in_dtype);
+  const size_t osz = dtype_size(out_dtype);
+  DynSrc dq = comm_dyn(c, 1);
+  if (push)
+    for (int p = 0; p < c->world; ++p)
+      if (p != c->rank) dq.mirror_delta[dq.mirror_n++] = (int64_t)((uintptr_t)c->peer[p] - (uintptr_t)c->base);
+  uint8_t* own = c->slot(c->base, push ? c->rank : 0);
+  const bool fdq_cfg = fdq_ok(cfg, in_dtype, out_dtype);
+  bool fdq_all = fdq_cfg;  // one epilogue setting per table: fuse only when every own piece can
+  std::vector<QJobSpec> q;
+  for (int k = 0; k < npieces; ++k) {
+    const int64_t gs = (int64_t)c->rank * rank_stride + pieces[k].offset;
+    qsdp_segment seg{gs, pieces[k].numel};
+    QJobSpec j = comm_qjob(pieces[k].src, seg, own + L.code_off[k], 0, *key, 0);
+    j.meta = reinterpret_cast<float*>(own + c->slot_codes + L.meta_off[k]);
+    uint8_t* o = static_cast<uint8_t*>(full_out) + (size_t)gs * osz;
+    if (!aligned(o, osz == 2 ? 8 : 16)) fdq_all = false;
+    j.dq_out = o;
+    q.push_back(j);
+  }
+  if (fdq_all) {
+    dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;
+    dq.dq_nocodes = c->world == 1 ? 1 : 0;
+  } else {
+    for (auto& j : q) j.dq_out = nullptr;
+  }
+  std::vector<DJobSpec> d;
+  for (int p = 0; p < c->world; ++p) {
+    if (fdq_all && p == c->rank) continue;
+    uint8_t* sl = push ? c->slot(c->base, p) : c->slot(c->peer[p], 0);
+    for (int k = 0; k < npieces; ++k) {
+      DJobSpec js;
+      memset(&js, 0, sizeof(DJobSpec));
+      js.codes[0] = sl + L.code_off[k];
+      js.meta[0] = reinterpret_cast<const float*>(sl + c->slot_codes + L.meta_off[k]);
+      js.nsrc = 1;
+      js.length = pieces[k].numel;
+      js.out = static_cast<uint8_t*>(full_out) + (size_t)((int64_t)p * rank_stride + pieces[k].offset) * osz;
+      d.push_back(js);
+    }
+  }
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
+  if (st != QSDP_OK) return st;
+  if (c->world > 1) {
+    st = comm_barrier(c, s);
+    if (st != QSDP_OK) return st;
+  }
+  if (d.empty()) return QSDP_OK;
+  return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0));
+}
+
+qsdp_status qsdp_reduce_scatter_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32_t npieces, int32_t in_dtype,
+                                       int64_t rank_stride, const qsdp_key* key, void* shard_out, int32_t out_dtype,
+                                       void* stream) {
+  if (c == nullptr || key == nullptr || shard_out == nullptr) return fail(QSDP_EINVAL, "null argument");
+  qsdp_status st = comm_failed(c);
+  if (st != QSDP_OK) return st;
+  const qsdp_qcfg* cfg = &c->g;
+  PieceLayout L;
+  st = piece_layout(c, cfg, pieces, npieces, L);
+  if (st != QSDP_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t isz = dtype_size(in_dtype), osz = dtype_size(out_dtype);
+  std::vector<QJobSpec> q;
+  for (int p = 0; p < c->world; ++p) {  // destination p's piece k -> owner p's slot [rank]
+    uint8_t* dst = c->slot(c->peer[p], c->rank);
+    for (int k = 0; k < npieces; ++k) {
+      qsdp_segment seg{(int64_t)p * rank_stride + pieces[k].offset, pieces[k].numel};
+      const void* x = static_cast<const uint8_t*>(pieces[k].src) + (size_t)((int64_t)p * rank_stride) * isz;
+      QJobSpec j = comm_qjob(x, seg, dst + L.code_off[k], 0, *key, (uint64_t)c->rank);
+      j.meta = reinterpret_cast<float*>(dst + c->slot_codes + L.meta_off[k]);
+      q.push_back(j);
+    }
+  }
+  DynSrc dq = comm_dyn(c, 1);
+  bool fdq1 = c->world == 1 && fdq_ok(cfg, in_dtype, out_dtype);
+  for (int k = 0; k < npieces && fdq1; ++k)
+    fdq1 = aligned(static_cast<uint8_t*>(shard_out) + (size_t)pieces[k].offset * osz, osz == 2 ? 8 : 16);
+  if (fdq1) {
+    for (int k = 0; k < npieces; ++k) q[k].dq_out = static_cast<uint8_t*>(shard_out) + (size_t)pieces[k].offset * osz;
+    dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;
+    dq.dq_add0 = 1;
+    dq.dq_nocodes = 1;
+  }
+  st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
+  if (st != QSDP_OK || fdq1) return st;
+  if (c->world > 1) {
+    st = comm_barrier(c, s);
+    if (st != QSDP_OK) return st;
+  }
+  std::vector<DJobSpec> d;
+  for (int k = 0; k < npieces; ++k) {
+    DJobSpec js;
+    memset(&js, 0, sizeof(DJobSpec));
+    for (int p = 0; p < c->world; ++p) {
+      uint8_t* sl = c->slot(c->base, p);
+      js.codes[p] = sl + L.code_off[k];
+      js.meta[p] = reinterpret_cast<const float*>(sl + c->slot_codes + L.meta_off[k]);
+    }
+    js.nsrc = c->world;
+    js.length = pieces[k].numel;
+    js.out = static_cast<uint8_t*>(shard_out) + (size_t)pieces[k].offset * osz;
+    d.push_back(js);
+  }
+  return run_dequant(d, cfg, 1, c->world, out_dtype, s, comm_dyn(c, 0));
+}
+
 qsdp_status qsdp_reduce_scatter_lattice(qsdp_comm* c, const void* full_grad, int32_t in_dtype, const qsdp_segment* segs,
                                         const qsdp_key* key, void* shard_out, int32_t out_dtype, void* x_shard,
                                         const qsdp_lattice* lat, void* stream) {

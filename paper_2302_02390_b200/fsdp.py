@@ -10,16 +10,32 @@ them on its dedicated all-gather and reduce-scatter streams, prefetching the
 next group's gather while the current group computes, so the quantized
 collectives overlap compute as in the paper.
 
-Keys follow the reference protocol: weights (root, step, group, phase, worker 0,
-start) with phase 0 in forward and 1 in the backward re-gather; gradients
-(root, step, group, PHASE_GRAD, rank, start).  The step is the host-side
-training step (:meth:`QSDPContext.next_step`).
+**Per-parameter protocol.**  FSDP2 flattens a group's parameters into one
+per-rank buffer: parameter k's dim-0-padded shard at a fixed offset, the same on
+every rank (``foreach_all_gather`` / ``foreach_reduce_scatter_copy_in``,
+torch/distributed/fsdp/_fully_shard/_fsdp_collectives.py:237-290, 667-675).
+The comms walk that layout (:func:`group_layout`) and treat each parameter as
+the reference treats a layer:
 
-FSDP2 flattens each group's parameters into one per-rank buffer (padded to
-equal shards), so the quantized buckets run over that flat buffer.
+* dense weights (2-D: linear / embedding matrices) are quantized -- weights with
+  the random-shift quantizer, gradients with the stochastic one -- keyed
+  (root, step, group, phase, worker, start) with ``start`` = the parameter
+  piece's offset in the gathered buffer (sharded.py:323-358, 386-413);
+* biases and norm parameters (1-D) travel at full precision (sharded.py:359-371,
+  414-429): a plain NCCL all-gather / AVG reduce-scatter of just those pieces,
+  the operation FSDP2 itself would run, so they are bit-identical to the
+  unquantized path.
+
+With ``param_dtype=bf16`` (bf16 compute, the FSDP2 mixed-precision baseline) the
+all-gather quantizes the fp32 master shard (``FSDPParam._sharded_param_data``,
+not FSDP2's bf16 copy-in) and writes the dequantized weights as bf16
+(RNE of the fp32 value == float32(reference fp64)); gradients are reduced in fp32
+(``reduce_dtype``).  Keys use the host step and the forward / backward phase.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
@@ -27,9 +43,36 @@ from torch.distributed.fsdp._fully_shard._fsdp_api import AllGather, ReduceScatt
 
 from .comm import QSDPComm, record_allgather, record_reducescatter
 from .quantize import QuantSpec, SegmentKey
-from .sharded import PHASE_GRAD, PHASE_W_BWD, PHASE_W_FWD, CommLedger, LedgerEntry
+from .sharded import PHASE_GRAD, PHASE_W_BWD, PHASE_W_FWD, CommLedger, LedgerEntry, Transfer
 
-__all__ = ["QSDPContext", "QSDPAllGather", "QSDPReduceScatter", "apply_qsdp"]
+__all__ = ["QSDPContext", "QSDPAllGather", "QSDPReduceScatter", "apply_qsdp", "group_layout", "ParamSlot"]
+
+
+@dataclass
+class ParamSlot:
+    """One parameter of a FSDP2 group in the per-rank flat buffer."""
+
+    name: str
+    offset: int      # element offset within a rank's flat shard
+    numel: int       # padded shard numel (identical on every rank)
+    dense: bool      # quantized (2-D weight) or full precision (bias / norm)
+    fsdp_param: object
+
+
+def group_layout(module) -> list[ParamSlot]:
+    """The flat layout FSDP2 all-gathers / reduce-scatters for ``module``'s group:
+    parameters in ``fsdp_params`` order, each its padded sharded numel."""
+    state = module._get_fsdp_state()
+    pg = state._fsdp_param_group
+    if pg is None:
+        return []
+    slots, off = [], 0
+    for fp in pg.fsdp_params:
+        n = fp.padded_sharded_param_size.numel()
+        name = getattr(getattr(fp, "_module_info", None), "param_name", "param")
+        slots.append(ParamSlot(name, off, n, len(fp._orig_size) >= 2, fp))
+        off += n
+    return slots
 
 
 class QSDPContext:
@@ -56,7 +99,10 @@ class QSDPContext:
         self.rs.set_sm_budget(sm_budget)
         self.step = 0
         self.phase = PHASE_W_FWD
-        self.calls = {"allgather": 0, "reducescatter": 0}
+        self.calls = {"allgather": 0, "reducescatter": 0, "raw_allgather": 0, "raw_reducescatter": 0}
+        self.layouts: dict[int, list[ParamSlot]] = {}
+        self.param_bits = None  # width of the full-precision all-gather (set from the param dtype)
+        self._idx: dict[tuple, torch.Tensor] = {}
         # the reference's per-step communication ledger (sharded.py:115-181)
         self.ledger = CommLedger()
         self.entry = LedgerEntry(step=0)
@@ -74,61 +120,176 @@ class QSDPContext:
         self.entry = LedgerEntry(step=self.step)
         self.phase = PHASE_W_FWD
 
+    def record(self, template: LedgerEntry) -> None:
+        """Add one collective's (cached) ledger records to the current step's entry."""
+        e = self.entry
+        e.transfers.extend(template.transfers)
+        e.allgather_bits += template.allgather_bits
+        e.reducescatter_bits += template.reducescatter_bits
+        e.allgather_payload_bits += template.allgather_payload_bits
+        e.reducescatter_payload_bits += template.reducescatter_payload_bits
+        e.allgather_events += 1 if template.allgather_events else 0
+        e.reducescatter_events += 1 if template.reducescatter_events else 0
+
+    def raw_index(self, layer: int, world: int, stride: int, device) -> tuple[torch.Tensor, int]:
+        """Flat positions of the full-precision pieces in a rank-major [world, stride] buffer
+        (cached): rank q's pieces in layout order."""
+        key = (layer, world, stride)
+        if key not in self._idx:
+            pos = []
+            for q in range(world):
+                for s in self.layouts[layer]:
+                    if not s.dense:
+                        pos.extend(range(q * stride + s.offset, q * stride + s.offset + s.numel))
+            self._idx[key] = torch.tensor(pos, dtype=torch.long, device=device)
+        idx = self._idx[key]
+        return idx, idx.numel() // world
+
     def close(self):
         self.ag.close()
         self.rs.close()
 
 
+class _LayerPlan:
+    """Per-(group, world) host state built on the first collective and reused: the C-ABI
+    piece arrays, the full-precision index tensors and the ledger records (FSDP2 drives
+    these comms from its Python hooks, so per-call host work is on the step's critical
+    path -- the 1.3B step is launch-bound)."""
+
+    def __init__(self, ctx: "QSDPContext", layer: int, world: int, stride: int, device, kind: str):
+        import ctypes
+        from . import _lib
+        slots = ctx.layouts[layer]
+        if sum(s.numel for s in slots) != stride:
+            raise ValueError("FSDP2 collective buffer does not match the group's parameter layout")
+        self.dense = [s for s in slots if s.dense and s.numel]
+        self.pieces = (_lib.Piece * max(1, len(self.dense)))()
+        for k, s in enumerate(self.dense):
+            self.pieces[k] = _lib.Piece(None, s.offset, s.numel)
+        self.masters = ()
+        self.idx, self.e = ctx.raw_index(layer, world, stride, device)
+        self.key = _lib.Key(ctx.root_seed, 0, layer, 0, 0)
+        self.keyp = ctypes.byref(self.key)
+        # the reference's ledger records of this collective (sharded.py:349-371, 403-429)
+        probe = LedgerEntry(step=0)
+        for s in self.dense:
+            if kind == "allgather":
+                record_allgather(probe, f"group{layer}.{s.name}", [(0, s.numel)] * world, ctx.wspec)
+            else:
+                record_reducescatter(probe, f"group{layer}.{s.name}", [(0, s.numel)] * world, ctx.gspec)
+        for s in slots:
+            if s.dense or not s.numel:
+                continue
+            if kind == "allgather":
+                width = 32 if ctx.param_bits is None else ctx.param_bits
+                for _ in range(world):
+                    probe.record(Transfer("allgather", f"group{layer}.{s.name}", width, s.numel * width // 8,
+                                          world - 1, s.numel * width))
+            else:
+                for _ in range(world - 1):
+                    probe.record(Transfer("reducescatter", f"group{layer}.{s.name}", 32, s.numel * 4, 1, s.numel * 32))
+        self.ledger = probe
+
+
 class QSDPAllGather(AllGather):
-    """Quantized all-gather of one FSDP2 group (C1)."""
+    """Quantized all-gather of one FSDP2 group (C1): the group's dense weights in one
+    group collective (qsdp_all_gather_pieces), biases / norms gathered at full precision."""
 
     def __init__(self, ctx: QSDPContext, layer: int):
         self.ctx, self.layer = ctx, layer
+        self.plans = {}
 
     def allocate(self, size, *, dtype, device):
         return torch.empty(*size, dtype=dtype, device=device)
 
     def __call__(self, output_tensor, input_tensor, group, async_op=False):
-        if input_tensor.dtype not in (torch.float32,):
-            raise ValueError("QSDP all-gather expects fp32 sharded parameters (param_dtype=None)")
-        world = group.size()
-        n = input_tensor.numel()
-        segs = [(p * n, n) for p in range(world)]
+        from . import _lib
+        from .quantize import _DTYPE_CODE
         c = self.ctx
-        c.ag.all_gather(input_tensor, segs, SegmentKey(c.root_seed, c.step, self.layer, c.phase, 0), output_tensor)
+        if output_tensor.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("QSDP all-gather writes fp32 or bf16 parameters")
+        world = group.size()
+        n_in = input_tensor.numel()
+        pl = self.plans.get((world, n_in))
+        if pl is None:
+            pl = self.plans[(world, n_in)] = _LayerPlan(c, self.layer, world, n_in, output_tensor.device, "allgather")
+        masters = tuple(s.fsdp_param._sharded_param_data for s in pl.dense)  # fp32 master shards
+        if masters != pl.masters:
+            for k, m in enumerate(masters):
+                if m.dtype != torch.float32 or m.numel() != pl.dense[k].numel:
+                    raise ValueError("QSDP all-gather expects fp32 sharded parameters")
+                pl.pieces[k].src = m.data_ptr()
+            pl.masters = masters
+        if pl.dense:
+            if c.wspec.inner != "levels":  # the group's dense weights: one quantize, barrier, dequant
+                pl.key.step, pl.key.phase = c.step, c.phase
+                _lib.check(_lib.lib().qsdp_all_gather_pieces(
+                    c.ag._h, pl.pieces, len(pl.dense), _lib.F32, n_in, pl.keyp, output_tensor.data_ptr(),
+                    _DTYPE_CODE[output_tensor.dtype], torch.cuda.current_stream().cuda_stream))
+            else:  # learned levels: one collective per weight
+                key = SegmentKey(c.root_seed, c.step, self.layer, c.phase, 0)
+                for m, s in zip(masters, pl.dense):
+                    c.ag.all_gather(m, [(q * n_in + s.offset, s.numel) for q in range(world)], key,
+                                    output_tensor[s.offset:])
+        if pl.e:  # full precision: what FSDP2 itself would gather for these parameters
+            send = input_tensor.index_select(0, pl.idx[:pl.e])
+            recv = torch.empty(world * pl.e, dtype=input_tensor.dtype, device=input_tensor.device)
+            dist.all_gather_into_tensor(recv, send, group=group)
+            output_tensor.index_copy_(0, pl.idx, recv)
+            c.calls["raw_allgather"] += 1
+        c.record(pl.ledger)
         c.calls["allgather"] += 1
-        record_allgather(c.entry, f"group{self.layer}", segs, c.wspec)
         return None
 
 
 class QSDPReduceScatter(ReduceScatter):
-    """Quantized reduce-scatter of one FSDP2 group's gradients (C2): average of the
-    dequantized contributions of every rank (sharded.py:375-433)."""
+    """Quantized reduce-scatter of one FSDP2 group's gradients (C2): the average of the
+    dequantized contributions of every rank (sharded.py:375-433) for the group's dense
+    weights in one group collective; biases / norms reduced at full precision."""
 
     def __init__(self, ctx: QSDPContext, layer: int):
         self.ctx, self.layer = ctx, layer
+        self.plans = {}
 
     def allocate(self, size, *, dtype, device):
         return torch.empty(*size, dtype=dtype, device=device)
 
     def __call__(self, output_tensor, input_tensor, group, op, async_op=False):
+        from . import _lib
         if op not in (dist.ReduceOp.AVG,) and getattr(op, "op", op) != dist.ReduceOp.AVG:
             raise ValueError("QSDP reduce-scatter computes the average (ReduceOp.AVG)")
-        if input_tensor.dtype != torch.float32:
+        if input_tensor.dtype != torch.float32 or output_tensor.dtype != torch.float32:
             raise ValueError("QSDP reduce-scatter expects fp32 gradients (reduce_dtype=float32)")
-        world = group.size()
-        n = output_tensor.numel()
-        segs = [(p * n, n) for p in range(world)]
         c = self.ctx
-        c.rs.reduce_scatter(input_tensor, segs, SegmentKey(c.root_seed, c.step, self.layer, PHASE_GRAD, c.rank),
-                            output_tensor)
+        world = group.size()
+        n_out = output_tensor.numel()
+        pl = self.plans.get((world, n_out))
+        if pl is None:
+            pl = self.plans[(world, n_out)] = _LayerPlan(c, self.layer, world, n_out, output_tensor.device,
+                                                         "reducescatter")
+        if pl.dense:
+            base = input_tensor.data_ptr()
+            for k, s in enumerate(pl.dense):
+                pl.pieces[k].src = base + 4 * s.offset
+            pl.key.step, pl.key.phase, pl.key.worker = c.step, PHASE_GRAD, c.rank
+            _lib.check(_lib.lib().qsdp_reduce_scatter_pieces(
+                c.rs._h, pl.pieces, len(pl.dense), _lib.F32, n_out, pl.keyp, output_tensor.data_ptr(), _lib.F32,
+                torch.cuda.current_stream().cuda_stream))
+        if pl.e:
+            send = input_tensor.index_select(0, pl.idx)
+            recv = torch.empty(pl.e, dtype=input_tensor.dtype, device=input_tensor.device)
+            dist.reduce_scatter_tensor(recv, send, op=dist.ReduceOp.AVG, group=group)
+            output_tensor.index_copy_(0, pl.idx[:pl.e], recv)
+            c.calls["raw_reducescatter"] += 1
+        c.record(pl.ledger)
         c.calls["reducescatter"] += 1
-        record_reducescatter(c.entry, f"group{self.layer}", segs, c.gspec)
         return None
 
 
-def apply_qsdp(modules, ctx: QSDPContext) -> None:
+def apply_qsdp(modules, ctx: QSDPContext, param_dtype=None) -> None:
     """Install QSDP comms on ``fully_shard``-ed modules (index = key ``layer``)."""
+    ctx.param_bits = None if param_dtype is None else torch.finfo(param_dtype).bits
     for i, m in enumerate(modules):
+        ctx.layouts[i] = group_layout(m)
         m.set_custom_all_gather(QSDPAllGather(ctx, i))
         m.set_custom_reduce_scatter(QSDPReduceScatter(ctx, i))

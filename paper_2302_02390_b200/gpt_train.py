@@ -45,30 +45,39 @@ def _shard_numel(params, world: int) -> int:
 
 
 def shard_model(model, mode: str, wspec: QuantSpec | None = None, gspec: QuantSpec | None = None,
-                root_seed: int = 0, weight_levels=None):
+                root_seed: int = 0, weight_levels=None, param_dtype=torch.bfloat16):
     """fully_shard every transformer block and the root; install QSDP comms if mode == 'qsdp'
-    (``weight_levels``: a LevelTable when ``wspec.inner == "levels"``)."""
+    (``weight_levels``: a LevelTable when ``wspec.inner == "levels"``).  Both modes use the
+    same mixed-precision policy: ``param_dtype`` all-gathered / computed parameters (bf16 by
+    default; QSDP quantizes the fp32 master shards and writes that dtype), fp32 gradient
+    reduce-scatter."""
     from torch.distributed.device_mesh import init_device_mesh
     from torch.distributed.fsdp import MixedPrecisionPolicy, fully_shard
 
     world = dist.get_world_size() if dist.is_initialized() else 1
     mesh = init_device_mesh("cuda", (world,))
-    mp = MixedPrecisionPolicy(param_dtype=None, reduce_dtype=torch.float32)
+    mp = MixedPrecisionPolicy(param_dtype=param_dtype, reduce_dtype=torch.float32)
     blocks = list(model.transformer.h)
-    block_params = [list(b.parameters()) for b in blocks]
-    inner = {id(p) for ps in block_params for p in ps}
-    root_params = [p for p in model.parameters() if id(p) not in inner]
-    max_shard = max([_shard_numel(ps, world) for ps in block_params] + [_shard_numel(root_params, world)])
+    # one QSDP group collective carries a group's dense parameters: slots sized for the
+    # largest group (codes padded per piece to 16 B, meta per piece to whole buckets)
+    bucket = max((wspec or QuantSpec(8, 1024, "shift")).bucket, (gspec or QuantSpec(8, 1024)).bucket)
+
+    def group_need(params):
+        dense = [p for p in params if p.dim() >= 2]
+        return _shard_numel(dense, world) + len(dense) * (bucket + 16)
+    inner_ids = {id(p) for b in blocks for p in b.parameters()}
+    max_shard = max([group_need(list(b.parameters())) for b in blocks] +
+                    [group_need([p for p in model.parameters() if id(p) not in inner_ids])])
     for b in blocks:
         fully_shard(b, mesh=mesh, mp_policy=mp, reshard_after_forward=True)
     fully_shard(model, mesh=mesh, mp_policy=mp, reshard_after_forward=True)
     ctx = None
     if mode == "qsdp":
         from .fsdp import QSDPContext, apply_qsdp
-        ctx = QSDPContext(max_shard + 4096, wspec or QuantSpec(8, 1024, "shift"),
+        ctx = QSDPContext(max_shard, wspec or QuantSpec(8, 1024, "shift"),
                           gspec or QuantSpec(8, 1024, "uniform_stochastic"), root_seed=root_seed,
                           device=torch.device("cuda", torch.cuda.current_device()), weight_levels=weight_levels)
-        apply_qsdp(blocks + [model], ctx)
+        apply_qsdp(blocks + [model], ctx, param_dtype)
     return ctx
 
 

@@ -111,6 +111,7 @@ def main():
         comm.close()
     failures += offset_views(rank, world, dev)
     failures += philox_collectives(rank, world, dev)
+    failures += group_pieces(rank, world, dev)
     failures += levels_all_gather(rank, world, dev)
     failures += lattice_reduce_scatter(rank, world, dev)
     failures += pipelined(rank, world, dev)
@@ -302,6 +303,51 @@ def philox_collectives(rank, world, dev):
                 and np.array_equal(sh[:n].cpu().numpy(), (acc / world).astype(np.float32))):
             fails += 1
             print(f"rank {rank} philox step {step}: mismatch", flush=True)
+    comm.close()
+    return fails
+
+
+def group_pieces(rank, world, dev):
+    """qsdp_all_gather_pieces / qsdp_reduce_scatter_pieces: several equal-per-rank pieces at
+    fixed offsets of a rank's flat buffer (an FSDP2 group), keyed start = q*stride + offset."""
+    fails = 0
+    rng = np.random.default_rng(23)
+    sizes = [5000, 1024 * 7, 333, 4096 * 3 + 8]
+    offs, off = [], 0
+    for n in sizes:
+        offs.append(off)
+        off += n + 5  # gaps: full-precision parameters of the group live there
+    stride = off
+    cap = sum(sizes) + len(sizes) * (1024 + 16)
+    comm = QSDPComm(cap, QuantSpec(8, 1024, "shift"), QuantSpec(8, 1024, "uniform_stochastic"))
+    shards = [[(rng.standard_normal(n) * 0.02).astype(np.float32) for n in sizes] for _ in range(world)]
+    grads = [(rng.standard_normal(world * stride) * 1e-3).astype(np.float32) for _ in range(world)]
+    for out_dt in (torch.float32, torch.bfloat16):
+        out = torch.zeros(world * stride, dtype=out_dt, device=dev)
+        pieces = [(torch.from_numpy(shards[rank][k]).to(dev), offs[k], sizes[k]) for k in range(len(sizes))]
+        comm.all_gather_pieces(pieces, stride, SegmentKey(2, 3, 4, 1, 0), out)
+        got = out.float().cpu().numpy()
+        for q in range(world):
+            for k, n in enumerate(sizes):
+                a = q * stride + offs[k]
+                c, m, _ = O.quantize_segment(shards[q][k], a, 1024, 8, 0, (2, 3, 4, 1, 0), 8)
+                exp = torch.from_numpy(O.dequantize_segment(c, m, n, 1024, 8, 8).astype(np.float32))
+                if not np.array_equal(got[a:a + n], exp.to(out_dt).float().numpy()):
+                    fails += 1
+                    print(f"rank {rank} pieces AG {out_dt} q {q} k {k}: mismatch", flush=True)
+    rs = torch.zeros(stride, device=dev)
+    comm.reduce_scatter_pieces(torch.from_numpy(grads[rank]).to(dev), list(zip(offs, sizes)), stride,
+                               SegmentKey(2, 3, 4, 2, rank), rs)
+    got = rs.cpu().numpy()
+    for k, n in enumerate(sizes):
+        a = rank * stride + offs[k]
+        acc = np.zeros(n)
+        for p in range(world):
+            c, m, _ = O.quantize_segment(grads[p][a:a + n], a, 1024, 8, 1, (2, 3, 4, 2, p), 8)
+            acc = acc + O.dequantize_segment(c, m, n, 1024, 8, 8)
+        if not np.array_equal(got[offs[k]:offs[k] + n], (acc / world).astype(np.float32)):
+            fails += 1
+            print(f"rank {rank} pieces RS k {k}: mismatch", flush=True)
     comm.close()
     return fails
 

@@ -129,3 +129,32 @@ def test_hierarchical_comm():
     dividing the world size, bit-exact vs the oracle (tests/dist_hier_check.py)."""
     n = min(8, torch.cuda.device_count())
     _torchrun("dist_hier_check.py", n, 29534)
+
+
+def test_group_pieces_world1(oracle):
+    """qsdp_all_gather_pieces / qsdp_reduce_scatter_pieces at world 1 (fused epilogue when
+    every piece is aligned, K3 otherwise)."""
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(31)
+    for sizes, gap in (([4096, 1024 * 3, 700], 0), ([5000, 2048, 129], 3)):
+        offs, off = [], 0
+        for n in sizes:
+            offs.append(off)
+            off += n + gap
+        comm = QSDPComm(sum(sizes) + len(sizes) * 1040, QuantSpec(8, 1024, "shift"),
+                        QuantSpec(4, 1024, "uniform_stochastic"), device=dev)
+        xs = [(rng.standard_normal(n) * 0.02).astype(np.float32) for n in sizes]
+        out = torch.zeros(off, device=dev)
+        comm.all_gather_pieces([(torch.from_numpy(x).to(dev), o, n) for x, o, n in zip(xs, offs, sizes)], off,
+                               SegmentKey(1, 2, 3, 0, 0), out)
+        g = (rng.standard_normal(off) * 1e-3).astype(np.float32)
+        rs = torch.zeros(off, device=dev)
+        comm.reduce_scatter_pieces(torch.from_numpy(g).to(dev), list(zip(offs, sizes)), off, SegmentKey(1, 2, 3, 2, 0), rs)
+        o, r = out.cpu().numpy(), rs.cpu().numpy()
+        for x, a, n in zip(xs, offs, sizes):
+            c, m, _ = oracle.quantize_segment(x, a, 1024, 8, 0, (1, 2, 3, 0, 0), 8)
+            assert np.array_equal(o[a:a + n], oracle.dequantize_segment(c, m, n, 1024, 8, 8).astype(np.float32))
+            c, m, _ = oracle.quantize_segment(g[a:a + n], a, 1024, 4, 1, (1, 2, 3, 2, 0), 8)
+            exp = (np.zeros(n) + oracle.dequantize_segment(c, m, n, 1024, 4, 8)) / 1
+            assert np.array_equal(r[a:a + n], exp.astype(np.float32))
+        comm.close()

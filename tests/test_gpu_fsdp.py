@@ -12,8 +12,9 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("ngpu", [1, 2])
+@pytest.mark.parametrize("ngpu", [2, 4])
 def test_fsdp2_qsdp_tracks_fsdp(ngpu):
+    """World >= 2 only: at world 1 FSDP2 runs no collective, so QSDP would never be exercised."""
     if torch.cuda.device_count() < ngpu:
         pytest.skip(f"needs {ngpu} GPUs")
     env = dict(os.environ, PYTHONPATH=ROOT)
