@@ -986,17 +986,17 @@ static QJobSpec comm_qjob(const void* x, const qsdp_segment& seg, uint8_t* slot,
 }
 
 // The push all-gather needs the quantizer that copies buckets out (the TMA32
-// kernel: direct widths, S % 8 == 0, 72 <= S, S * sizeof(T) <= 8 KB).
+// kernel: direct widths, S % 8 == 0, 72 <= S, S * sizeof(T) <= 16 KB).
 static bool push_ok(const qsdp_comm* c, const qsdp_qcfg* cfg, int in_dtype) {
   const bool direct = cfg->bits == 2 || cfg->bits == 4 || cfg->bits == 8 || cfg->bits == 16;
   const int isz = in_dtype == QSDP_F64 ? 8 : 4;
   return c->world > 1 && cfg->inner != QSDP_INNER_LEVELS &&
          (cfg->noise == QSDP_NOISE_PCG64_SEEDSEQ || cfg->inner == QSDP_INNER_SHIFT) && direct &&
-         cfg->bucket % 8 == 0 && cfg->bucket >= 72 && cfg->bucket * isz <= 8192;
+         cfg->bucket % 8 == 0 && cfg->bucket >= 72 && cfg->bucket * isz <= 16384;
 }
 
 // The fused dequant epilogue lives in the TMA32 quantizer: direct widths,
-// S % 8 == 0, a whole warp per bucket (S >= 72), S * sizeof(T) <= 8 KB
+// S % 8 == 0, a whole warp per bucket (S >= 72), S * sizeof(T) <= 16 KB
 // (launch_q_t's routing), an fp32 / fp64 / bf16 output.
 static bool fdq_ok(const qsdp_qcfg* cfg, int in_dtype, int out_dtype) {
   static const bool off = getenv("QSDP_NO_FDQ") != nullptr && getenv("QSDP_NO_FDQ")[0] == '1';  // A/B switch
@@ -1005,7 +1005,7 @@ static bool fdq_ok(const qsdp_qcfg* cfg, int in_dtype, int out_dtype) {
   const int isz = in_dtype == QSDP_F64 ? 8 : 4;
   return cfg->inner != QSDP_INNER_LEVELS &&
          (cfg->noise == QSDP_NOISE_PCG64_SEEDSEQ || cfg->inner == QSDP_INNER_SHIFT) && direct && cfg->bucket % 8 == 0 &&
-         cfg->bucket >= 72 && cfg->bucket * isz <= 8192 &&
+         cfg->bucket >= 72 && cfg->bucket * isz <= 16384 &&
          (out_dtype == QSDP_F32 || out_dtype == QSDP_F64 || out_dtype == QSDP_BF16);
 }
 

@@ -451,7 +451,7 @@ __device__ __forceinline__ BucketRef resolve_q(const QJobTable& tab, int64_t b, 
 
 // ---------------------------------------------------------------------------
 // K1/K2 fast path: TMA-pipelined quantizer for the direct widths.
-// Requirements (host-checked): BITS in {2,4,8,16}, S % 8 == 0, S*sizeof(T) <= 8 KB.
+// Requirements (host-checked): BITS in {2,4,8,16}, S % 8 == 0, S*sizeof(T) <= 8 KB (16 KB for the TMA32 kernel).
 // Dynamic smem: [warps][NST] stages of TEAMS*S elements, then [warps][NST] mbarriers.
 // ---------------------------------------------------------------------------
 template <typename T, int INNER, int BITS, int TL, int NST>
@@ -2036,7 +2036,14 @@ cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
   constexpr int NST = 2;
   const size_t stage = (size_t)tab.bucket * sizeof(T);
   int wpc = 8;
-  while (wpc > 2 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
+  if (stage <= 8192) {
+    while (wpc > 2 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
+  } else {  // 16 KB buckets (S = 4096 fp32): two CTAs per SM, each as many warps' rings as fit in
+            // ~100 KB (3 warps: measured 3.7 / 1.4 TB/s K1 / K2 vs 3.3 / 1.2 with one 6-warp CTA)
+    const size_t per_warp = NST * stage + NST * sizeof(uint64_t) + 32 * sizeof(SeedOut);
+    wpc = (int)((100 * 1024 - 33 * sizeof(JumpEntry)) / per_warp);
+    wpc = wpc < 1 ? 1 : (wpc > 8 ? 8 : wpc);
+  }
   const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t) +
                       (size_t)wpc * 32 * sizeof(SeedOut) + (INNER == 1 ? 33 * sizeof(JumpEntry) : 0);
   auto kern = quantize_tma32_kernel<T, INNER, BITS, NST, FDQ>;
@@ -2082,7 +2089,7 @@ cudaError_t launch_q_tma(const QJobTable& tab, bool vec, int sms, cudaStream_t s
 template <typename T, int INNER, int TL>
 cudaError_t launch_q_tl(const QJobTable& tab, bool vec, int sms, cudaStream_t s) {
   const int S = tab.bucket;
-  if (S * (int)sizeof(T) <= 8192) {
+  if (S * (int)sizeof(T) <= (TL == 32 ? 16384 : 8192)) {
     switch (tab.bits) {
       case 8: return launch_q_tma<T, INNER, 8, TL>(tab, vec, sms, s);
       case 4: return launch_q_tma<T, INNER, 4, TL>(tab, vec, sms, s);

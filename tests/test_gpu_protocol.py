@@ -88,3 +88,37 @@ def test_protocol_semantics():
     _, e = one.train_step(0)
     assert e.allgather_bits == 0 and e.reducescatter_bits == 0
     assert e.allgather_events == 2 * len(one.layers) and e.reducescatter_events == len(one.layers)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_criterion7_gpu_hooks_100_steps(P):
+    """Acceptance criterion 7 (pkg/tests/test_acceptance.py:258-290) through the product hooks:
+    widths (64, 64, 10), batch 32, lr 0.05, w8/g8 bucket 1024, seeds 11, 100 steps.  The
+    collectives run on the GPU; the MLP's matmuls stay on the host (numpy), so the run is
+    compared bit-for-bit with the oracle-hooked run on this box and with the reference's
+    golden run (tests/golden/golden_mlp100.npz) when this host's BLAS reproduces it."""
+    import os
+    import mlp_workload as W
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_mlp100.npz"))
+    kw = dict(widths=(64, 64, 10), P=P, batch=32, lr=0.05,
+              quant=QuantConfig(weight_bits=8, gradient_bits=8, bucket_size=1024), seed=11)
+    runs = {}
+    for hooks in ("gpu", "oracle"):
+        sim = W.make(hooks, **kw)
+        losses, ag, rs = [], [], []
+        for t in range(100):
+            loss, e = sim.train_step(t)
+            losses.append(loss)
+            ag.append(e.allgather_bits)
+            rs.append(e.reducescatter_bits)
+        runs[hooks] = (losses, ag, rs, sim.full_params())
+    (lg, agg, rsg, pg), (lo, ago, rso, po) = runs["gpu"], runs["oracle"]
+    assert lg == lo and agg == ago and rsg == rso
+    assert all(np.array_equal(pg[k], po[k]) for k in pg)
+    assert agg == list(g[f"P{P}_bits"][0]) and rsg == list(g[f"P{P}_bits"][1])  # ledger: exact always
+    same_blas = lo == list(g[f"P{P}_losses"])
+    for name, v in pg.items():
+        if same_blas:
+            assert np.array_equal(v, g[f"P{P}_param_{name}"]), name
+        else:  # only the host matmuls can differ from the reference host
+            assert np.allclose(v, g[f"P{P}_param_{name}"], rtol=1e-9, atol=1e-12), name

@@ -1,6 +1,8 @@
 """CPU: pin the C oracle against the reference's golden vectors, its own
 known-answer tests, and (when mounted) the live reference."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -240,3 +242,24 @@ def test_philox_live_reference_random(oracle, reference):
         codes, meta, _ = oracle.quantize_segment(v, start, n, bits, inner, key, 1, noise=1)
         assert np.array_equal(oracle.unpack(codes, n, bits), blk.codes), t
         assert (float(meta[0, 0]), float(meta[0, 1]), float(meta[0, 2])) == (blk.shift, blk.scale_lo, blk.scale_hi), t
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_criterion7_oracle_hooks_100_steps(P):
+    """Acceptance criterion 7 (test_acceptance.py:258-290) through the oracle-hooked
+    workload: 100 steps bit-identical to the reference's ShardedMLP / ReferenceMLP golden run."""
+    import mlp_workload as W
+    from paper_2302_02390_b200.sharded import QuantConfig
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_mlp100.npz"))
+    sim = W.make("oracle", widths=(64, 64, 10), P=P, batch=32, lr=0.05,
+                 quant=QuantConfig(weight_bits=8, gradient_bits=8, bucket_size=1024), seed=11)
+    losses, ag, rs = [], [], []
+    for t in range(100):
+        loss, e = sim.train_step(t)
+        losses.append(loss)
+        ag.append(e.allgather_bits)
+        rs.append(e.reducescatter_bits)
+    assert losses == list(g[f"P{P}_losses"])
+    assert ag == list(g[f"P{P}_bits"][0]) and rs == list(g[f"P{P}_bits"][1])
+    for name, v in sim.full_params().items():
+        assert np.array_equal(v, g[f"P{P}_param_{name}"]), name
