@@ -149,6 +149,20 @@ qsdp_status qsdp_quantize_batch(const qsdp_qitem* items, int32_t nitems, int32_t
 qsdp_status qsdp_quantize_batch_dstep(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
                                       const qsdp_qcfg* cfg, uint64_t* d_bad, const uint64_t* d_step,
                                       void* stream);
+/* Shared-generator bucketing (bucketed_quantize with one rng, quantize.py:289-313; the theory
+ * side's UniformStochasticGradientQuantizer, optimizer.py:177-191): bucket j's draws continue
+ * ONE numpy PCG64 stream.  d_states[4*j..4*j+3] = (state_lo, state_hi, inc_lo, inc_hi) of the
+ * stream before bucket j's first draw (the caller's prefix sum: 1 draw per non-degenerate
+ * shift bucket, n per non-degenerate stochastic bucket, 0 for a degenerate one).  Input must
+ * be finite (the caller raises first, as the reference does).  d_scratch: length uint32. */
+qsdp_status qsdp_quantize_stream(const void* x, int32_t x_dtype, int64_t length, const qsdp_qcfg* cfg,
+                                 const uint64_t* d_states, uint8_t* codes, float* meta, uint32_t* d_scratch,
+                                 void* stream);
+/* quantize_with_levels(v, table, stochastic=True, rng) (quantize.py:400-422) on device fp64
+ * values: element i draws the i-th double of the numpy PCG64 stream whose state before the
+ * first draw is state[4] = (state_lo, state_hi, inc_lo, inc_hi) (host memory); nlevels >= 2. */
+qsdp_status qsdp_levels_stochastic(const double* d_values, int64_t n, const double* d_levels, int32_t nlevels,
+                                   const uint64_t* state, uint32_t* d_codes, void* stream);
 /* *d_counter += delta on the stream (advances a device step counter inside a graph). */
 qsdp_status qsdp_counter_add(uint64_t* d_counter, uint64_t delta, void* stream);
 

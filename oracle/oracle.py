@@ -76,6 +76,8 @@ def lib():
         L.qo_quantize_segment_f32_nz.argtypes = qargs + [i32]
         L.qo_quantize_segment_f32_nz.restype = i64
         L.qo_philox_rng.argtypes = [vp, u64, u64, u64, u64, u64, u64]
+        L.qo_quantize_shared.argtypes = [vp, i64, i64, i32, i32, vp, vp, vp]
+        L.qo_quantize_shared.restype = i64
         L.qo_philox_next.argtypes = [vp]
         L.qo_philox_next.restype = u64
         L.qo_quantize_segment_f32.restype = i64
@@ -140,6 +142,19 @@ class Philox:
 
 
 NOISE = {"pcg64": 0, "philox": 1}
+
+
+def quantize_shared(v, bucket, bits, inner, state: int, inc: int):
+    """bucketed_quantize with one shared numpy PCG64 stream (quantize.py:289-313) from
+    (state, inc); returns (packed codes, meta, bad index, final (state, inc))."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    n = v.size
+    g = np.array([state >> 64, state & (2**64 - 1), inc >> 64, inc & (2**64 - 1)], dtype=np.uint64)
+    codes = np.zeros(max(codes_bytes(n, bucket, bits), 1), dtype=np.uint8)
+    meta = np.zeros((max(num_buckets(n, bucket), 1), 3), dtype=np.float32)
+    bad = lib().qo_quantize_shared(_ptr(v), n, bucket, bits, inner, _ptr(g), _ptr(codes), _ptr(meta))
+    return (codes[: codes_bytes(n, bucket, bits)], meta[: num_buckets(n, bucket)], int(bad),
+            ((int(g[0]) << 64) | int(g[1]), (int(g[2]) << 64) | int(g[3])))
 
 
 # -- per-bucket / per-segment quantizer -------------------------------------------

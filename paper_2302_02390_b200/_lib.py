@@ -45,7 +45,7 @@ EXPORTED_SYMBOLS = (
     "qsdp_wire_parse", "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes",
     "qsdp_unpack_codes", "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice",
     "qsdp_comm_set_sm_budget", "qsdp_comm_set_timeout", "qsdp_comm_status", "qsdp_all_gather_pieces",
-    "qsdp_reduce_scatter_pieces",
+    "qsdp_reduce_scatter_pieces", "qsdp_quantize_stream", "qsdp_levels_stochastic",
 )
 
 
@@ -159,6 +159,8 @@ def lib():
     L.qsdp_comm_set_sm_budget.argtypes = [vp, i32]
     L.qsdp_comm_set_timeout.argtypes = [vp, i64]
     L.qsdp_comm_status.argtypes = [vp]
+    L.qsdp_quantize_stream.argtypes = [vp, i32, i64, cfgp, vp, vp, vp, vp, vp]
+    L.qsdp_levels_stochastic.argtypes = [vp, i64, vp, i32, vp, vp, vp]
     L.qsdp_all_gather_pieces.argtypes = [vp, ctypes.POINTER(Piece), i32, i32, i64, keyp, vp, i32, vp]
     L.qsdp_reduce_scatter_pieces.argtypes = [vp, ctypes.POINTER(Piece), i32, i32, i64, keyp, vp, i32, vp]
     L.qsdp_wire_parse.argtypes = [vp, i64, ctypes.POINTER(WireInfo)]
@@ -196,7 +198,8 @@ def lib():
                  "qsdp_learn_levels", "qsdp_comm_set_weight_levels", "qsdp_wire_parse",
                  "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes", "qsdp_unpack_codes",
                  "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice", "qsdp_comm_set_sm_budget",
-                 "qsdp_comm_set_timeout", "qsdp_comm_status", "qsdp_all_gather_pieces", "qsdp_reduce_scatter_pieces"):
+                 "qsdp_comm_set_timeout", "qsdp_comm_status", "qsdp_all_gather_pieces", "qsdp_reduce_scatter_pieces",
+                 "qsdp_quantize_stream", "qsdp_levels_stochastic"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib

@@ -32,6 +32,11 @@ namespace qsdp {
 cudaError_t launch_quantize_f32(const QJobTable& tab, bool vec, int sms, cudaStream_t s);
 cudaError_t launch_quantize_f64(const QJobTable& tab, bool vec, int sms, cudaStream_t s);
 cudaError_t launch_quantize_philox(const QJobTable& tab, bool f64, bool vec, int sms, cudaStream_t s);
+cudaError_t launch_levels_stochastic(const double* v, int64_t n, const double* q, int nl, const uint64_t* state,
+                                     uint32_t* codes, cudaStream_t s);
+cudaError_t launch_quantize_stream(const void* x, bool f64, int64_t length, int S, int bits, int inner,
+                                   const uint64_t* states, uint32_t* scratch, uint8_t* codes, int64_t codes_bytes,
+                                   float* meta, int sms, cudaStream_t s);
 cudaError_t launch_dequant(const DJobTable& tab, bool vec, int sms, cudaStream_t s);
 cudaError_t upload_jump_f32(const JumpEntry* host);
 cudaError_t upload_jump_f64(const JumpEntry* host);
@@ -394,6 +399,39 @@ qsdp_status qsdp_quantize_batch_dstep(const qsdp_qitem* items, int32_t nitems, i
 }
 
 static bool pow2(int64_t v) { return v >= 1 && (v & (v - 1)) == 0; }
+
+qsdp_status qsdp_levels_stochastic(const double* d_values, int64_t n, const double* d_levels, int32_t nlevels,
+                                   const uint64_t* state, uint32_t* d_codes, void* stream) {
+  if (n < 0 || nlevels < 2 || state == nullptr) return fail(QSDP_EINVAL, "need n >= 0, >= 2 levels and a stream state");
+  if (n > 0 && (d_values == nullptr || d_levels == nullptr || d_codes == nullptr)) return fail(QSDP_EINVAL, "null buffer");
+  int sms = 0;
+  qsdp_status st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  cudaError_t e = launch_levels_stochastic(d_values, n, d_levels, nlevels, state, d_codes,
+                                           reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "stochastic levels launch");
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_quantize_stream(const void* x, int32_t x_dtype, int64_t length, const qsdp_qcfg* cfg,
+                                 const uint64_t* d_states, uint8_t* codes, float* meta, uint32_t* d_scratch,
+                                 void* stream) {
+  qsdp_status st = check_cfg(cfg);
+  if (st != QSDP_OK) return st;
+  if (cfg->noise != QSDP_NOISE_PCG64_SEEDSEQ) return fail(QSDP_EINVAL, "a shared stream replays numpy PCG64");
+  if (x_dtype != QSDP_F32 && x_dtype != QSDP_F64) return fail(QSDP_EINVAL, "input dtype must be f32 or f64");
+  if (length < 0) return fail(QSDP_EINVAL, "negative length");
+  if (length > 0 && (x == nullptr || d_states == nullptr || codes == nullptr || meta == nullptr || d_scratch == nullptr))
+    return fail(QSDP_EINVAL, "null buffer");
+  int sms = 0;
+  st = ensure_device(sms);
+  if (st != QSDP_OK) return st;
+  cudaError_t e = launch_quantize_stream(x, x_dtype == QSDP_F64, length, cfg->bucket, cfg->bits, cfg->inner, d_states,
+                                         d_scratch, codes, qsdp_codes_bytes(length, cfg), meta, sms,
+                                         reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "stream quantize launch");
+  return QSDP_OK;
+}
 
 qsdp_status qsdp_quantize_levels_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
                                        const qsdp_qcfg* cfg, const double* d_levels, int32_t nlevels,

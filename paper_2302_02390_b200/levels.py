@@ -108,14 +108,15 @@ def learn_levels(values, initial: LevelTable, learning_rate: float = 0.01) -> Le
 
 
 def quantize_with_levels(v, table: LevelTable, stochastic: bool = False, rng=None):
-    """Map values to level indices, clamping outside the table's span
-    (quantize.py:400-422; deterministic mode).  Returns codes in the input's
-    container type (numpy uint32 for array-likes, int64 CUDA tensor for tensors)."""
+    """Map values to level indices, clamping outside the table's span (quantize.py:400-422).
+    Returns codes in the input's container type (numpy uint32 for array-likes, int64 CUDA
+    tensor for tensors).  ``stochastic=True`` rounds to the bracketing levels with the draws
+    of ``rng`` (a numpy PCG64 Generator, continued on the device and advanced by v.size
+    draws, as the reference's rng.random(v.size))."""
     if stochastic:
         if rng is None:
             raise ValueError("stochastic mode requires an rng")
-        raise NotImplementedError("stochastic level rounding is not used by the QSDP path "
-                                  "(quantize_bucket calls stochastic=False)")
+        return _levels_stochastic(v, table, rng)
     is_t = isinstance(v, torch.Tensor)
     x = _as_device_f64(v)
     q = table.device(x.device)
@@ -125,6 +126,29 @@ def quantize_with_levels(v, table: LevelTable, stochastic: bool = False, rng=Non
         x = torch.clamp(x, q[0], q[-1])
         mids = (q[:-1] + q[1:]) / 2
         codes = torch.searchsorted(mids, x, side="left")
+    return codes if is_t else codes.cpu().numpy().astype(np.uint32)
+
+
+def _levels_stochastic(v, table: LevelTable, rng):
+    is_t = isinstance(v, torch.Tensor)
+    x = _as_device_f64(v)
+    n = x.numel()
+    q = table.device(x.device)
+    if q.numel() == 1:  # the reference returns before drawing
+        codes = torch.zeros(n, dtype=torch.int64, device=x.device)
+        return codes if is_t else codes.cpu().numpy().astype(np.uint32)
+    bg = rng.bit_generator
+    if not isinstance(bg, np.random.PCG64):
+        raise TypeError("stochastic levels replay a numpy PCG64 Generator (np.random.default_rng)")
+    st = bg.state["state"]
+    state, inc = int(st["state"]), int(st["inc"])
+    words = (ctypes.c_uint64 * 4)(state & 0xFFFFFFFFFFFFFFFF, state >> 64, inc & 0xFFFFFFFFFFFFFFFF, inc >> 64)
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=x.device)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.lib().qsdp_levels_stochastic(x.data_ptr(), n, q.data_ptr(), q.numel(), words, out.data_ptr(),
+                                                     _stream(x.device)))
+    bg.advance(n)
+    codes = out[:n].to(torch.int64)
     return codes if is_t else codes.cpu().numpy().astype(np.uint32)
 
 

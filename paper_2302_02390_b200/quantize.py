@@ -354,8 +354,80 @@ def _device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def quantize_bucket(values, bit_width: int, inner: str, rng: KeyedBucketRNG, levels=None) -> QuantizedBlock:
-    """Min-max normalise one bucket and quantize it on the GPU (quantize.py:235-286)."""
+_PCG_M = 0x2360ED051FC65DA44385DF649FCCF645
+_MASK128 = (1 << 128) - 1
+
+
+def _pcg_advance_coeffs(k: int):
+    """(A_k, G_k) with state_k = A_k * state + G_k * inc (mod 2^128): numpy PCG64 after k draws."""
+    am, ap, cm, cp = 1, 0, _PCG_M, 1
+    while k:
+        if k & 1:
+            am = am * cm & _MASK128
+            ap = (ap * cm + cp) & _MASK128
+        cp = (cm + 1) * cp & _MASK128
+        cm = cm * cm & _MASK128
+        k >>= 1
+    return am, ap
+
+
+def _shared_stream_blocks(v: np.ndarray, bucket: int, bit_width: int, inner: str, rng) -> list:
+    """bucketed_quantize with ONE numpy Generator consumed in bucket order (quantize.py:289-313):
+    a non-degenerate bucket draws 1 (shift) or n (stochastic) outputs, a degenerate bucket none
+    (quantize.py:256-264).  The prefix sum of draws gives every bucket's starting PCG64 state;
+    the device quantizes all buckets at once from those states, and ``rng`` is advanced past
+    the draws, exactly where the reference leaves it."""
+    bg = rng.bit_generator
+    if not isinstance(bg, np.random.PCG64):
+        raise TypeError("a shared generator must be numpy PCG64 (np.random.default_rng): the device replays its stream")
+    if not 1 <= bit_width <= 16:
+        raise ValueError(f"bit_width must be in [1, 16], got {bit_width}")
+    n = v.size
+    starts = np.arange(0, n, bucket)
+    lens = np.minimum(bucket, n - starts)
+    bad = np.flatnonzero(~np.isfinite(v))
+    nb = starts.size if bad.size == 0 else int(bad[0] // bucket)  # buckets quantized before a raise
+    lo = np.minimum.reduceat(v, starts).astype(np.float32) if n else np.zeros(0, np.float32)
+    hi = np.maximum.reduceat(v, starts).astype(np.float32) if n else np.zeros(0, np.float32)
+    draws = np.where(lo == hi, 0, 1 if inner == "shift" else lens).astype(np.int64)
+    st = bg.state["state"]
+    state, inc = int(st["state"]), int(st["inc"])
+    common = int(draws.max()) if draws.size else 0
+    a_c, g_c = _pcg_advance_coeffs(common)
+    words = np.zeros((max(nb, 1), 4), dtype=np.uint64)
+    cur = state
+    for j in range(nb):
+        words[j] = (cur & 0xFFFFFFFFFFFFFFFF, cur >> 64, inc & 0xFFFFFFFFFFFFFFFF, inc >> 64)
+        d = int(draws[j])
+        if d:
+            a, g = (a_c, g_c) if d == common else _pcg_advance_coeffs(d)
+            cur = (a * cur + g * inc) & _MASK128
+    if bad.size:  # the reference consumed the earlier buckets' draws, then raised in _check_finite
+        bg.advance(int(draws[:nb].sum()))
+        i = int(bad[0])
+        raise ValueError(f"non-finite bucket value at index {i - nb * bucket}: {v[i]!r}")
+    dev = _device()
+    spec = QuantSpec(bit_width, bucket, inner)
+    cfg = spec.cfg()
+    x = torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+    states = torch.from_numpy(words.view(np.int64)).to(dev)
+    codes = torch.empty(max(codes_bytes(n, spec), 1), dtype=torch.uint8, device=dev)
+    meta = torch.empty((max(num_buckets(n, bucket), 1), 3), dtype=torch.float32, device=dev)
+    scratch = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().qsdp_quantize_stream(x.data_ptr(), _lib.F64, n, ctypes.byref(cfg), states.data_ptr(),
+                                                   codes.data_ptr(), meta.data_ptr(), scratch.data_ptr(),
+                                                   _stream(dev)))
+    blocks = _blocks_from_device(codes, meta, n, bucket, bit_width)
+    bg.advance(int(draws.sum()))
+    return blocks
+
+
+def quantize_bucket(values, bit_width: int, inner: str, rng, levels=None) -> QuantizedBlock:
+    """Min-max normalise one bucket and quantize it on the GPU (quantize.py:235-286).
+
+    ``rng``: a ``bucket_rng`` / ``philox_rng`` key (the device regenerates the keyed stream),
+    or a numpy PCG64 Generator, whose stream the device continues (and advances)."""
     v = np.asarray(values, dtype=float)
     if v.size == 0:
         raise ValueError("cannot quantize an empty bucket")
@@ -363,6 +435,8 @@ def quantize_bucket(values, bit_width: int, inner: str, rng: KeyedBucketRNG, lev
         raise ValueError(f"unknown inner mode {inner!r}")
     if inner == "levels":  # no draws: rng is not consulted (quantize.py:275-279)
         return _levels_blocks(v, v.size, bit_width, levels)[0]
+    if isinstance(rng, np.random.Generator):
+        return _shared_stream_blocks(v, v.size, bit_width, inner, rng)[0]
     if not isinstance(rng, KeyedBucketRNG):
         raise TypeError("rng must come from bucket_rng(...): the device reproduces keyed streams")
     spec = QuantSpec(bit_width, v.size, inner, rng.noise)
@@ -375,9 +449,11 @@ def bucketed_quantize(v, bucket: BucketSpec, bit_width: int, inner: str = "shift
                       levels=None) -> list:
     """Split into buckets and quantize each (quantize.py:289-313).
 
-    ``rng`` must be a ``bucket_rng(...)`` key: bucket j is then keyed with
-    ``start + j*bucket_size`` exactly like ``_segment_blocks`` (sharded.py:243-248).
-    A shared sequential numpy Generator is not reproduced on the device.
+    ``rng`` = a numpy PCG64 Generator (or None: ``np.random.default_rng()``, as the
+    reference): ONE stream shared by the buckets in order, replayed on the device and
+    advanced like the reference's; or a ``bucket_rng(...)`` / ``philox_rng(...)`` key:
+    bucket j keyed with ``start + j*bucket_size`` exactly like ``_segment_blocks``
+    (sharded.py:243-248).
     """
     v = np.atleast_1d(np.asarray(v, dtype=float))
     if v.size == 0:
@@ -386,8 +462,14 @@ def bucketed_quantize(v, bucket: BucketSpec, bit_width: int, inner: str = "shift
         raise ValueError(f"bit_width must be in [1, 16], got {bit_width}")
     if inner == "levels":
         return _levels_blocks(v, bucket.bucket_size, bit_width, levels)
+    if inner not in INNER_MODES:
+        raise ValueError(f"unknown inner mode {inner!r}")
+    if rng is None:
+        rng = np.random.default_rng()
+    if isinstance(rng, np.random.Generator):
+        return _shared_stream_blocks(v, bucket.bucket_size, bit_width, inner, rng)
     if not isinstance(rng, KeyedBucketRNG):
-        raise TypeError("rng must come from bucket_rng(...)")
+        raise TypeError("rng must be a numpy PCG64 Generator or come from bucket_rng(...)")
     spec = QuantSpec(bit_width, bucket.bucket_size, inner, rng.noise)
     x = torch.from_numpy(np.ascontiguousarray(v)).to(_device())
     codes, meta = quantize_segment(x, rng.start, spec, rng.key, check_finite=True)

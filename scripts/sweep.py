@@ -3,9 +3,12 @@
 
 Each point is 10 back-to-back calls of one collective captured in a CUDA graph,
 timed with CUDA events after an L2 flush, max over ranks.  Reported per point:
-effective GB/s = 4N / T (the nccl-tests algbw convention on the fp32 tensor) and
-the fraction of the roofline T* = max(HBM bytes / 6555.2 GB/s, NVLink bytes /
-900 GB/s) with the per-element bytes of §8(d):
+effective GB/s = 4N / T (the nccl-tests algbw convention on the fp32 tensor), bus
+GB/s = c N (P-1)/P / T against 900 GB/s per direction, the fraction of the roofline
+T* = max(HBM bytes / peak, NVLink bytes / 900 GB/s) (HBM peak from MEASURED_PEAKS.json)
+with the per-element bytes of §8(d), and -- counter evidence -- the NVLink data
+bytes rank 0's GPU transmitted during the timed replays (nvidia-smi nvlink -gt d,
+read before / after) per collective, next to the algorithmic c N (P-1)/P:
 
     C1 all-gather       HBM 4/P + o + 2c     NVLink c (P-1)/P
     C2 reduce-scatter   HBM 4 + 2c + 4/P     NVLink c (P-1)/P      (c = b/8 + 12/S, o = 4)
@@ -23,7 +26,25 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2302_02390_b200.comm import PipelinedComm, QSDPComm, plan_segments  # noqa: E402
 from paper_2302_02390_b200.quantize import QuantSpec, SegmentKey, advance_counter  # noqa: E402
 
-HBM, NVL = 6555.2e9, 900e9
+NVL = 900e9
+try:
+    HBM = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                            "MEASURED_PEAKS.json")))["hbm_gbs"]) * 1e9
+except Exception:
+    HBM = 6555.2e9  # B200_PROFILING.md fallback
+
+
+def nvlink_tx_bytes(index: int):
+    """Data bytes this GPU has transmitted over all its NVLinks (nvidia-smi nvlink -gt d), or None."""
+    import re
+    import subprocess
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(index)], capture_output=True,
+                             text=True, timeout=30).stdout
+    except Exception:
+        return None
+    tx = [int(m) for m in re.findall(r"Data Tx:\s*(\d+)\s*KiB", out)]
+    return sum(tx) * 1024 if tx else None
 
 
 def main():
@@ -69,6 +90,7 @@ def main():
                 torch.cuda.synchronize()
                 tot = 0.0
                 reps = 5
+                tx0 = nvlink_tx_bytes(local) if (rank == 0 and world > 1) else None
                 for r in range(reps):
                     flush.fill_(r)
                     if world > 1:
@@ -80,6 +102,7 @@ def main():
                     b.record()
                     torch.cuda.synchronize()
                     tot += a.elapsed_time(b)
+                tx1 = nvlink_tx_bytes(local) if tx0 is not None else None
                 t = torch.tensor([tot / reps / 10 * 1e-3], device=dev, dtype=torch.float64)  # s per collective
                 if world > 1:
                     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -89,10 +112,16 @@ def main():
                 nvl = c * (P - 1) / P
                 tstar = max(hbm * n / HBM, nvl * n / NVL)
                 if rank == 0:
-                    print(json.dumps({"P": P, "pipe": pipe, "n": n, "mb_fp32": n * 4 / 2 ** 20, "bits": bits, "collective": kind,
-                                      "us": round(T * 1e6, 2), "eff_gbs": round(4 * n / T / 1e9, 1),
-                                      "roofline_eff_gbs": round(4 * n / tstar / 1e9, 1),
-                                      "frac_of_roofline": round(tstar / T, 3)}), flush=True)
+                    line = {"P": P, "pipe": pipe, "n": n, "mb_fp32": n * 4 / 2 ** 20, "bits": bits, "collective": kind,
+                            "us": round(T * 1e6, 2), "eff_gbs": round(4 * n / T / 1e9, 1),
+                            "bus_gbs": round(nvl * n / T / 1e9, 1), "bus_frac_of_900": round(nvl * n / T / NVL, 3),
+                            "roofline_eff_gbs": round(4 * n / tstar / 1e9, 1),
+                            "frac_of_roofline": round(tstar / T, 3), "hbm_peak_gbs": round(HBM / 1e9, 1)}
+                    if tx1 is not None:
+                        per = (tx1 - tx0) / (reps * 10)
+                        line["nvlink_tx_bytes_per_collective"] = int(per)
+                        line["nvlink_tx_algorithmic_bytes"] = int(nvl * n)
+                    print(json.dumps(line), flush=True)
             comm.close()
         del x, g, full, shard
         torch.cuda.empty_cache()

@@ -263,3 +263,18 @@ def test_criterion7_oracle_hooks_100_steps(P):
     assert ag == list(g[f"P{P}_bits"][0]) and rs == list(g[f"P{P}_bits"][1])
     for name, v in sim.full_params().items():
         assert np.array_equal(v, g[f"P{P}_param_{name}"]), name
+
+
+def test_shared_generator_golden(oracle):
+    """bucketed_quantize with one Generator across buckets (quantize.py:289-313):
+    codes, scales and where the stream is left, vs the reference goldens."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_shared.npz"))
+    for i, (bits, inner, S, n, seed) in enumerate(g["sh_cases"]):
+        bg = np.random.PCG64(int(seed))
+        st = bg.state["state"]
+        codes, meta, bad, (s2, inc2) = oracle.quantize_shared(g[f"sh_{i}_x"], int(S), int(bits), int(inner),
+                                                              int(st["state"]), int(st["inc"]))
+        assert bad == -1
+        assert np.array_equal(codes, g[f"sh_{i}_codes"]) and np.array_equal(meta, g[f"sh_{i}_meta"]), i
+        bg.state = {"bit_generator": "PCG64", "state": {"state": s2, "inc": inc2}, "has_uint32": 0, "uinteger": 0}
+        assert int(bg.random_raw()) == int(g[f"sh_{i}_next"][0]), i
