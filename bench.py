@@ -268,6 +268,10 @@ def trace_step(g, flush, path):
     from torch.profiler import ProfilerActivity, profile
     flush.fill_(7)
     torch.cuda.synchronize()
+    if not path:
+        g.replay()
+        torch.cuda.synchronize()
+        return
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         g.replay()
         torch.cuda.synchronize()
@@ -538,8 +542,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    if args.trace and rank == 0:
-        trace_step(g_step, flush, args.trace)
+    if args.trace:  # every rank replays (the collectives' barriers need all of them); rank 0 records
+        barrier()
+        trace_step(g_step, flush, args.trace if rank == 0 else "")
+        barrier()
     value = world * 12.0 * N_total / (ms_step * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel: per-kind graphs timed with CUDA events ----
