@@ -1,0 +1,6 @@
+set -o pipefail
+python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r2_gputest.log 2>&1; tail -2 gpurun_out/r2_gputest.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1; tail -1 gpurun_out/r2_smoke.log
+python bench.py > gpurun_out/r2_bench_n1.json 2> gpurun_out/r2_bench_n1.err; tail -c 400 gpurun_out/r2_bench_n1.json
+python bench.py --steps 2 --warmup 3 --no-gpt --no-e2e --no-cpu-baseline --no-levels > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r2_ncu_launches_n1.csv python bench.py --steps 2 --warmup 3 --no-gpt --no-e2e --no-cpu-baseline --no-levels > gpurun_out/r2_ncu_bench.log 2>&1; echo "launches rc=$?"
+python scripts/prof_fused.py --reps 1 > /dev/null 2>&1 && ncu --set full --import-source on --clock-control none -k regex:quantize_tma32 -c 2 -o gpurun_out/r2_ncu_fused python scripts/prof_fused.py --reps 1 > gpurun_out/r2_ncu_fused.log 2>&1; echo "full rc=$?"

@@ -11,7 +11,7 @@ HOT = {"K1 quantize (shift)", "K2 quantize (stochastic)", "K3 dequantize", "K4 d
 
 
 def label(name: str) -> str:
-    if "quantize_tma32_kernel" in name or "fused_collective_kernel" in name or "quantize_tma_kernel" in name:
+    if "quantize_tma32_kernel" in name or "quantize_tma_kernel" in name or "quantize_kernel" in name:
         inner = name.split("<")[1].split(",")[1].strip()
         return "K1 quantize (shift)" if inner in ("0", "(int)0") else "K2 quantize (stochastic)"
     if "dequant_kernel" in name or "dequant_fast" in name:
