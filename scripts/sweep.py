@@ -58,7 +58,7 @@ def main():
     S = 1024
     flush = torch.empty(64 << 20, dtype=torch.int32, device=dev)
     ctr = torch.zeros(1, dtype=torch.int64, device=dev)
-    for logn in (18, 20, 22, 24, 26, 28):
+    for logn in [int(v) for v in os.environ.get("SWEEP_LOGN", "18,20,22,24,26,28").split(",")]:
         n = 1 << logn
         segs = plan_segments(n, world, S)
         s0, ns = segs[rank]
@@ -66,7 +66,7 @@ def main():
         g = torch.randn(n, device=dev) * 1e-3
         full = torch.empty(n, device=dev)
         shard = torch.empty(max(ns, 1), device=dev)
-        for bits in (8, 4):
+        for bits in [int(v) for v in os.environ.get("SWEEP_BITS", "8,4").split(",")]:
             pipe = int(os.environ.get("PIPE", "0"))  # >1: PipelinedComm with this many chunks
             ctor = (lambda *a, **k: PipelinedComm(*a, chunks=pipe, **k)) if pipe > 1 else QSDPComm
             comm = ctor(max(m for _, m in segs), QuantSpec(bits, S, "shift"), QuantSpec(bits, S, "uniform_stochastic"),
