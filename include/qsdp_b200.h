@@ -311,6 +311,11 @@ qsdp_status qsdp_reduce_scatter_lattice(qsdp_comm* c, const void* full_grad, int
 typedef struct {
   const void* src;
   int64_t offset, numel;
+  int32_t raw;       /* non-zero: a full-precision piece (bias / norm, sharded.py:359-371, 414-429):
+                        all-gather -- every rank's piece cast (RNE) to out_dtype; reduce-scatter --
+                        out = (0.0 + v_0 + ... + v_{P-1}) / P in fp64, ranks in order, rounded once.
+                        Carried by the collective's barrier kernel (at most 48 per call). */
+  int32_t reserved;
 } qsdp_piece;
 qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32_t npieces, int32_t in_dtype,
                                    int64_t rank_stride, const qsdp_key* key, void* full_out, int32_t out_dtype,

@@ -50,7 +50,8 @@ EXPORTED_SYMBOLS = (
 
 
 class Piece(ctypes.Structure):
-    _fields_ = [("src", ctypes.c_void_p), ("offset", ctypes.c_int64), ("numel", ctypes.c_int64)]
+    _fields_ = [("src", ctypes.c_void_p), ("offset", ctypes.c_int64), ("numel", ctypes.c_int64),
+                ("raw", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class QCfg(ctypes.Structure):

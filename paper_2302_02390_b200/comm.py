@@ -219,14 +219,17 @@ class QSDPComm:
     @staticmethod
     def _pieces(pieces):
         arr = (_lib.Piece * len(pieces))()
-        for k, (src, off, n) in enumerate(pieces):
-            arr[k] = _lib.Piece(src.data_ptr() if src is not None else None, int(off), int(n))
+        for k, pc in enumerate(pieces):
+            src, off, n = pc[:3]
+            raw = 1 if len(pc) > 3 and pc[3] else 0
+            arr[k] = _lib.Piece(src.data_ptr() if src is not None else None, int(off), int(n), raw, 0)
         return arr
 
     def all_gather_pieces(self, pieces, rank_stride: int, key: SegmentKey, out: torch.Tensor,
                           in_dtype=torch.float32) -> torch.Tensor:
         """C1 over a group of pieces in one call: ``pieces`` = [(this rank's piece tensor, offset,
-        numel)]; rank q's piece k lands at ``out[q * rank_stride + offset]`` (keyed start)."""
+        numel[, raw])]; rank q's piece k lands at ``out[q * rank_stride + offset]`` (keyed start).
+        ``raw`` pieces travel at full precision (cast to ``out.dtype``, sharded.py:359-371)."""
         arr = self._pieces(pieces)
         k = key.c()
         with torch.cuda.device(self.device):
@@ -238,12 +241,15 @@ class QSDPComm:
     def reduce_scatter_pieces(self, grad: torch.Tensor, pieces, rank_stride: int, key: SegmentKey,
                               out: torch.Tensor) -> torch.Tensor:
         """C2 over a group of pieces: ``grad`` is this rank's rank-major gradient
-        [world * rank_stride]; ``pieces`` = [(offset, numel)]; ``out[offset]`` receives piece k's
-        average."""
+        [world * rank_stride]; ``pieces`` = [(offset, numel[, raw])]; ``out[offset]`` receives
+        piece k's average (``raw``: of the full-precision values, fp64 in rank order,
+        sharded.py:414-429)."""
         arr = (_lib.Piece * len(pieces))()
         esz = grad.element_size()
-        for j, (off, n) in enumerate(pieces):
-            arr[j] = _lib.Piece(grad.data_ptr() + int(off) * esz, int(off), int(n))
+        for j, pc in enumerate(pieces):
+            off, n = pc[:2]
+            raw = 1 if len(pc) > 2 and pc[2] else 0
+            arr[j] = _lib.Piece(grad.data_ptr() + int(off) * esz, int(off), int(n), raw, 0)
         k = key.c()
         with torch.cuda.device(self.device):
             _lib.check(_lib.lib().qsdp_reduce_scatter_pieces(

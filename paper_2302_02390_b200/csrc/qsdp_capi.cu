@@ -14,6 +14,7 @@
 // Slots are double-buffered by call parity, so one barrier per collective
 // suffices: a rank rewrites parity k's slots only after every peer has passed
 // the barrier of call k+1, i.e. finished reading call k-1's data.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -794,6 +795,126 @@ __global__ void qsdp_barrier_kernel(PeerFlags pf, int rank, int world, unsigned 
   if (t == 0) *reinterpret_cast<volatile unsigned long long*>(epoch_ptr) = target;
 }
 
+// ---------------------------------------------------------------------------
+// Full-precision pieces of a group collective (biases / norms: sharded.py:359-371,
+// 414-429) ride on the barrier kernel: pushed into the peers' slots before its arrive,
+// copied out (all-gather) or averaged in rank order (reduce-scatter) after its wait --
+// no extra launch and no separate collective for them.
+// ---------------------------------------------------------------------------
+constexpr int kMaxRaw = 48;
+struct RawPieceDev {
+  const uint8_t* src;  // all-gather: this rank's piece; reduce-scatter: destination 0's piece
+  int64_t n;           // elements
+  int64_t slot_off;    // byte offset of the piece's values in a slot
+  int64_t out_off;     // element offset in the output (all-gather: + q * stride)
+};
+struct RawTable {
+  int32_t n, mode;             // pieces; 0 all-gather, 1 reduce-scatter
+  int32_t in_dt, out_dt;       // qsdp_dtype
+  int32_t world, rank;
+  int64_t stride;              // rank_stride (elements)
+  int64_t slot_bytes, parity_stride;
+  uint8_t* out;
+  uint8_t* own_slots;                      // own slot 0, parity 0
+  uint8_t* peer_slot[QSDP_MAX_WORLD];      // slot [rank] of rank p's workspace, parity 0 (own: base)
+  RawPieceDev p[kMaxRaw];
+};
+
+__device__ __forceinline__ int dt_size(int dt) { return dt == QSDP_F64 ? 8 : dt == QSDP_BF16 ? 2 : 4; }
+__device__ __forceinline__ double raw_ld(const uint8_t* b, int dt, int64_t i) {
+  if (dt == QSDP_F64) return reinterpret_cast<const double*>(b)[i];
+  if (dt == QSDP_BF16) return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(b)[i]);
+  return (double)reinterpret_cast<const float*>(b)[i];
+}
+__device__ __forceinline__ void raw_st(uint8_t* b, int dt, int64_t i, double v) {  // round to nearest even
+  if (dt == QSDP_F64) reinterpret_cast<double*>(b)[i] = v;
+  else if (dt == QSDP_BF16) reinterpret_cast<__nv_bfloat16*>(b)[i] = __double2bfloat16(v);
+  else reinterpret_cast<float*>(b)[i] = __double2float_rn(v);
+}
+
+// before the arrive: all-gather -- cast this rank's piece to the output dtype into its own
+// output slice and into slot [rank] of every peer; reduce-scatter -- destination q's piece
+// (input dtype, unchanged) into slot [rank] of owner q.
+__device__ void raw_push(const RawTable& rt, int64_t par) {
+  const int nt = blockDim.x;
+  for (int k = 0; k < rt.n; ++k) {
+    const RawPieceDev& pc = rt.p[k];
+    for (int q = 0; q < rt.world; ++q) {
+      if (rt.mode == 0) {
+        uint8_t* dst = q == rt.rank ? rt.out + (size_t)(rt.rank * rt.stride + pc.out_off) * dt_size(rt.out_dt)
+                                    : rt.peer_slot[q] + par + pc.slot_off;
+        for (int64_t i = threadIdx.x; i < pc.n; i += nt) raw_st(dst, rt.out_dt, i, raw_ld(pc.src, rt.in_dt, i));
+      } else {
+        const uint8_t* src = pc.src + (size_t)(q * rt.stride) * dt_size(rt.in_dt);
+        uint8_t* dst = rt.peer_slot[q] + par + pc.slot_off;
+        const int es = dt_size(rt.in_dt);
+        for (int64_t i = threadIdx.x; i < pc.n * es / 2; i += nt)
+          reinterpret_cast<uint16_t*>(dst)[i] = reinterpret_cast<const uint16_t*>(src)[i];
+      }
+    }
+  }
+}
+
+// after the wait: all-gather -- peers' pieces from own slots into the output; reduce-scatter
+// -- out = (0.0 + v_0 + v_1 + ... + v_{P-1}) / P in fp64, sources in rank order, rounded once.
+__device__ void raw_post(const RawTable& rt, int64_t par) {
+  const int nt = blockDim.x;
+  for (int k = 0; k < rt.n; ++k) {
+    const RawPieceDev& pc = rt.p[k];
+    if (rt.mode == 0) {
+      const int es = dt_size(rt.out_dt);
+      for (int q = 0; q < rt.world; ++q) {
+        if (q == rt.rank) continue;
+        const uint8_t* src = rt.own_slots + (size_t)q * rt.slot_bytes + par + pc.slot_off;
+        uint8_t* dst = rt.out + (size_t)(q * rt.stride + pc.out_off) * es;
+        for (int64_t i = threadIdx.x; i < pc.n * es / 2; i += nt)
+          reinterpret_cast<uint16_t*>(dst)[i] = reinterpret_cast<const uint16_t*>(src)[i];
+      }
+    } else {
+      uint8_t* dst = rt.out + (size_t)pc.out_off * dt_size(rt.out_dt);
+      for (int64_t i = threadIdx.x; i < pc.n; i += nt) {
+        double acc = 0.0;
+        for (int q = 0; q < rt.world; ++q)
+          acc = __dadd_rn(acc, raw_ld(rt.own_slots + (size_t)q * rt.slot_bytes + par + pc.slot_off, rt.in_dt, i));
+        raw_st(dst, rt.out_dt, i, __ddiv_rn(acc, (double)rt.world));
+      }
+    }
+  }
+}
+
+// The flag barrier with the full-precision pieces (world 1: the pieces only, no flags).
+__global__ void __launch_bounds__(512) qsdp_barrier_raw_kernel(PeerFlags pf, unsigned long long* epoch_ptr,
+                                                               unsigned long long* err_word,
+                                                               unsigned long long timeout_ns, RawTable rt) {
+  const int t = threadIdx.x;
+  const int rank = rt.rank, world = rt.world;
+  const unsigned long long target =
+      world > 1 ? *reinterpret_cast<volatile unsigned long long*>(epoch_ptr) + 1ull : 0ull;
+  const int64_t par = world > 1 ? (int64_t)(target & 1ull) * rt.parity_stride : 0;
+  raw_push(rt, par);
+  __threadfence_system();
+  __syncthreads();
+  if (world > 1 && t < world) {
+    unsigned long long* dst = pf.flags[t] + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(target) : "memory");
+    const unsigned long long* mine = pf.flags[rank] + t;
+    const unsigned long long t0 = globaltimer_ns();
+    unsigned long long v = 0;
+    for (unsigned it = 0;; ++it) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+      if (v >= target) break;
+      if ((it & 255u) == 255u && globaltimer_ns() - t0 > timeout_ns) {
+        atomicCAS(err_word, 0ull, (unsigned long long)(t + 1) | (target << 8));
+        __threadfence_system();
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  raw_post(rt, par);
+  if (t == 0 && world > 1) *reinterpret_cast<volatile unsigned long long*>(epoch_ptr) = target;
+}
+
 __global__ void qsdp_counter_add_kernel(unsigned long long* p, unsigned long long delta) { *p += delta; }
 
 struct qsdp_comm {
@@ -1183,25 +1304,72 @@ static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int3
 // after all codes -- the same on every rank, derived from the piece list alone.
 // ---------------------------------------------------------------------------
 struct PieceLayout {
-  std::vector<size_t> code_off, meta_off;
+  std::vector<size_t> code_off, meta_off;  // quantized: codes / meta; full precision: values (in code_off)
   size_t codes = 0, meta = 0;
+  int ndense = 0, nraw = 0;
 };
 
+// raw_esz: bytes per full-precision element in a slot (all-gather: output dtype, values
+// pre-cast; reduce-scatter: input dtype).  Quantized pieces first, then the raw values.
 static qsdp_status piece_layout(const qsdp_comm* c, const qsdp_qcfg* cfg, const qsdp_piece* pieces, int32_t np,
-                                PieceLayout& L) {
+                                size_t raw_esz, PieceLayout& L) {
   if (np < 1 || pieces == nullptr) return fail(QSDP_EINVAL, "need at least one piece");
-  L.code_off.resize(np);
-  L.meta_off.resize(np);
+  L.code_off.assign(np, 0);
+  L.meta_off.assign(np, 0);
   for (int k = 0; k < np; ++k) {
     if (pieces[k].numel < 0 || pieces[k].offset < 0) return fail(QSDP_EINVAL, "negative piece");
     if (pieces[k].numel > 0 && pieces[k].src == nullptr) return fail(QSDP_EINVAL, "null piece input");
+    if (pieces[k].raw) {
+      if (pieces[k].numel > 0) ++L.nraw;
+      continue;
+    }
+    ++L.ndense;
     L.code_off[k] = L.codes;
     L.meta_off[k] = L.meta;
     L.codes += round_up((size_t)qsdp_codes_bytes(pieces[k].numel, cfg), 16);
     L.meta += (size_t)qsdp_num_buckets(pieces[k].numel, cfg->bucket) * 12;
   }
+  if (L.nraw > kMaxRaw) return fail(QSDP_EINVAL, "more than 48 full-precision pieces in one group collective");
+  for (int k = 0; k < np; ++k)
+    if (pieces[k].raw && pieces[k].numel > 0) {
+      L.code_off[k] = L.codes;
+      L.codes += round_up((size_t)pieces[k].numel * raw_esz, 16);
+    }
   if (L.codes > c->slot_codes || L.meta > c->slot_meta)
     return fail(QSDP_EINVAL, "group pieces exceed the communicator's slot (max_segment_elems)");
+  return QSDP_OK;
+}
+
+// The barrier of a group collective, carrying its full-precision pieces (world 1 with raw
+// pieces: the kernel without flags; world 1 without: nothing).
+static qsdp_status pieces_barrier(qsdp_comm* c, const qsdp_piece* pieces, int32_t np, const PieceLayout& L, int mode,
+                                  int32_t in_dtype, int32_t out_dtype, int64_t stride, void* out, cudaStream_t s) {
+  if (L.nraw == 0) return c->world > 1 ? comm_barrier(c, s) : QSDP_OK;
+  PeerFlags pf;
+  memset(&pf, 0, sizeof(pf));
+  for (int j = 0; j < c->world; ++j) {
+    if (c->peer[j] == nullptr) return fail(QSDP_EPEER, "peers not opened");
+    pf.flags[j] = reinterpret_cast<unsigned long long*>(c->peer[j]);
+  }
+  RawTable rt;
+  memset(&rt, 0, sizeof(rt));
+  rt.mode = mode;
+  rt.in_dt = in_dtype;
+  rt.out_dt = out_dtype;
+  rt.world = c->world;
+  rt.rank = c->rank;
+  rt.stride = stride;
+  rt.slot_bytes = (int64_t)c->slot_bytes;
+  rt.parity_stride = c->world > 1 ? c->parity_stride() : 0;
+  rt.out = static_cast<uint8_t*>(out);
+  rt.own_slots = c->slot(c->base, 0);
+  for (int p = 0; p < c->world; ++p) rt.peer_slot[p] = c->slot(c->peer[p], c->rank);
+  for (int k = 0; k < np; ++k)
+    if (pieces[k].raw && pieces[k].numel > 0)
+      rt.p[rt.n++] = RawPieceDev{static_cast<const uint8_t*>(pieces[k].src), pieces[k].numel,
+                                 (int64_t)L.code_off[k], pieces[k].offset};
+  qsdp_barrier_raw_kernel<<<1, 512, 0, s>>>(pf, c->epoch(), c->err_dev, c->timeout_ns, rt);
+  QSDP_CUDA(cudaGetLastError());
   return QSDP_OK;
 }
 
@@ -1212,13 +1380,14 @@ qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32
   qsdp_status st = comm_failed(c);
   if (st != QSDP_OK) return st;
   const qsdp_qcfg* cfg = &c->w;
-  if (cfg->inner == QSDP_INNER_LEVELS) return fail(QSDP_EINVAL, "group collectives take affine weight specs");
+  const size_t osz = dtype_size(out_dtype);
   PieceLayout L;
-  st = piece_layout(c, cfg, pieces, npieces, L);
+  st = piece_layout(c, cfg, pieces, npieces, osz, L);
   if (st != QSDP_OK) return st;
+  if (cfg->inner == QSDP_INNER_LEVELS && L.ndense > 0)
+    return fail(QSDP_EINVAL, "group collectives quantize with affine weight specs (levels: full-precision pieces only)");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool push = push_ok(c, cfg, in_dtype);
-  const size_t osz = dtype_size(out_dtype);
   DynSrc dq = comm_dyn(c, 1);
   if (push)
     for (int p = 0; p < c->world; ++p)
@@ -1228,6 +1397,7 @@ qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32
   bool fdq_all = fdq_cfg;  // one epilogue setting per table: fuse only when every own piece can
   std::vector<QJobSpec> q;
   for (int k = 0; k < npieces; ++k) {
+    if (pieces[k].raw) continue;
     const int64_t gs = (int64_t)c->rank * rank_stride + pieces[k].offset;
     qsdp_segment seg{gs, pieces[k].numel};
     QJobSpec j = comm_qjob(pieces[k].src, seg, own + L.code_off[k], 0, *key, 0);
@@ -1248,6 +1418,7 @@ qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32
     if (fdq_all && p == c->rank) continue;
     uint8_t* sl = push ? c->slot(c->base, p) : c->slot(c->peer[p], 0);
     for (int k = 0; k < npieces; ++k) {
+      if (pieces[k].raw) continue;
       DJobSpec js;
       memset(&js, 0, sizeof(DJobSpec));
       js.codes[0] = sl + L.code_off[k];
@@ -1258,12 +1429,12 @@ qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32
       d.push_back(js);
     }
   }
-  st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
-  if (st != QSDP_OK) return st;
-  if (c->world > 1) {
-    st = comm_barrier(c, s);
+  if (!q.empty()) {
+    st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
     if (st != QSDP_OK) return st;
   }
+  st = pieces_barrier(c, pieces, npieces, L, 0, in_dtype, out_dtype, rank_stride, full_out, s);
+  if (st != QSDP_OK) return st;
   if (d.empty()) return QSDP_OK;
   return run_dequant(d, cfg, 0, 1, out_dtype, s, comm_dyn(c, 0));
 }
@@ -1275,15 +1446,18 @@ qsdp_status qsdp_reduce_scatter_pieces(qsdp_comm* c, const qsdp_piece* pieces, i
   qsdp_status st = comm_failed(c);
   if (st != QSDP_OK) return st;
   const qsdp_qcfg* cfg = &c->g;
+  const size_t isz = dtype_size(in_dtype), osz = dtype_size(out_dtype);
   PieceLayout L;
-  st = piece_layout(c, cfg, pieces, npieces, L);
+  st = piece_layout(c, cfg, pieces, npieces, isz, L);
   if (st != QSDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t isz = dtype_size(in_dtype), osz = dtype_size(out_dtype);
   std::vector<QJobSpec> q;
+  std::vector<int> dense;  // piece index of each quantized piece
+  for (int k = 0; k < npieces; ++k)
+    if (!pieces[k].raw) dense.push_back(k);
   for (int p = 0; p < c->world; ++p) {  // destination p's piece k -> owner p's slot [rank]
     uint8_t* dst = c->slot(c->peer[p], c->rank);
-    for (int k = 0; k < npieces; ++k) {
+    for (int k : dense) {
       qsdp_segment seg{(int64_t)p * rank_stride + pieces[k].offset, pieces[k].numel};
       const void* x = static_cast<const uint8_t*>(pieces[k].src) + (size_t)((int64_t)p * rank_stride) * isz;
       QJobSpec j = comm_qjob(x, seg, dst + L.code_off[k], 0, *key, (uint64_t)c->rank);
@@ -1293,22 +1467,23 @@ qsdp_status qsdp_reduce_scatter_pieces(qsdp_comm* c, const qsdp_piece* pieces, i
   }
   DynSrc dq = comm_dyn(c, 1);
   bool fdq1 = c->world == 1 && fdq_ok(cfg, in_dtype, out_dtype);
-  for (int k = 0; k < npieces && fdq1; ++k)
-    fdq1 = aligned(static_cast<uint8_t*>(shard_out) + (size_t)pieces[k].offset * osz, osz == 2 ? 8 : 16);
+  for (int k : dense)
+    if (fdq1) fdq1 = aligned(static_cast<uint8_t*>(shard_out) + (size_t)pieces[k].offset * osz, osz == 2 ? 8 : 16);
   if (fdq1) {
-    for (int k = 0; k < npieces; ++k) q[k].dq_out = static_cast<uint8_t*>(shard_out) + (size_t)pieces[k].offset * osz;
+    for (size_t i = 0; i < dense.size(); ++i)
+      q[i].dq_out = static_cast<uint8_t*>(shard_out) + (size_t)pieces[dense[i]].offset * osz;
     dq.dq_dtype = out_dtype == QSDP_F32 ? 0 : out_dtype == QSDP_F64 ? 1 : 2;
     dq.dq_add0 = 1;
     dq.dq_nocodes = 1;
   }
-  st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
-  if (st != QSDP_OK || fdq1) return st;
-  if (c->world > 1) {
-    st = comm_barrier(c, s);
+  if (!q.empty()) {
+    st = run_quantize(q, in_dtype, cfg, nullptr, s, dq);
     if (st != QSDP_OK) return st;
   }
+  st = pieces_barrier(c, pieces, npieces, L, 1, in_dtype, out_dtype, rank_stride, shard_out, s);
+  if (st != QSDP_OK || fdq1 || dense.empty()) return st;
   std::vector<DJobSpec> d;
-  for (int k = 0; k < npieces; ++k) {
+  for (int k : dense) {
     DJobSpec js;
     memset(&js, 0, sizeof(DJobSpec));
     for (int p = 0; p < c->world; ++p) {

@@ -22,9 +22,12 @@ the reference treats a layer:
   (root, step, group, phase, worker, start) with ``start`` = the parameter
   piece's offset in the gathered buffer (sharded.py:323-358, 386-413);
 * biases and norm parameters (1-D) travel at full precision (sharded.py:359-371,
-  414-429): a plain NCCL all-gather / AVG reduce-scatter of just those pieces,
-  the operation FSDP2 itself would run, so they are bit-identical to the
-  unquantized path.
+  414-429) inside the same group collective (``qsdp_piece.raw``): the all-gather
+  casts each rank's fp32 master piece to the parameter dtype (RNE, the cast FSDP2's
+  copy-in does, so these are bit-identical to the unquantized path), the
+  reduce-scatter averages the ranks' contributions in rank order in fp64 and rounds
+  once (the reference's ``acc + vals ... / P``).  One C call, one barrier per
+  group: no separate NCCL collective and no host-side gather/scatter of the pieces.
 
 With ``param_dtype=bf16`` (bf16 compute, the FSDP2 mixed-precision baseline) the
 all-gather quantizes the fp32 master shard (``FSDPParam._sharded_param_data``,
@@ -35,6 +38,7 @@ not FSDP2's bf16 copy-in) and writes the dequantized weights as bf16
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass
 
 import torch
@@ -99,10 +103,10 @@ class QSDPContext:
         self.rs.set_sm_budget(sm_budget)
         self.step = 0
         self.phase = PHASE_W_FWD
-        self.calls = {"allgather": 0, "reducescatter": 0, "raw_allgather": 0, "raw_reducescatter": 0}
+        self.calls = {"allgather": 0, "reducescatter": 0}
+        self.host_s = {"allgather": 0.0, "reducescatter": 0.0}  # host time inside the comm hooks
         self.layouts: dict[int, list[ParamSlot]] = {}
         self.param_bits = None  # width of the full-precision all-gather (set from the param dtype)
-        self._idx: dict[tuple, torch.Tensor] = {}
         # the reference's per-step communication ledger (sharded.py:115-181)
         self.ledger = CommLedger()
         self.entry = LedgerEntry(step=0)
@@ -131,20 +135,6 @@ class QSDPContext:
         e.allgather_events += 1 if template.allgather_events else 0
         e.reducescatter_events += 1 if template.reducescatter_events else 0
 
-    def raw_index(self, layer: int, world: int, stride: int, device) -> tuple[torch.Tensor, int]:
-        """Flat positions of the full-precision pieces in a rank-major [world, stride] buffer
-        (cached): rank q's pieces in layout order."""
-        key = (layer, world, stride)
-        if key not in self._idx:
-            pos = []
-            for q in range(world):
-                for s in self.layouts[layer]:
-                    if not s.dense:
-                        pos.extend(range(q * stride + s.offset, q * stride + s.offset + s.numel))
-            self._idx[key] = torch.tensor(pos, dtype=torch.long, device=device)
-        idx = self._idx[key]
-        return idx, idx.numel() // world
-
     def close(self):
         self.ag.close()
         self.rs.close()
@@ -152,9 +142,9 @@ class QSDPContext:
 
 class _LayerPlan:
     """Per-(group, world) host state built on the first collective and reused: the C-ABI
-    piece arrays, the full-precision index tensors and the ledger records (FSDP2 drives
+    piece array (quantized and full-precision pieces) and the ledger records (FSDP2 drives
     these comms from its Python hooks, so per-call host work is on the step's critical
-    path -- the 1.3B step is launch-bound)."""
+    path -- the 1.3B step is host-bound)."""
 
     def __init__(self, ctx: "QSDPContext", layer: int, world: int, stride: int, device, kind: str):
         import ctypes
@@ -162,17 +152,20 @@ class _LayerPlan:
         slots = ctx.layouts[layer]
         if sum(s.numel for s in slots) != stride:
             raise ValueError("FSDP2 collective buffer does not match the group's parameter layout")
-        self.dense = [s for s in slots if s.dense and s.numel]
-        self.pieces = (_lib.Piece * max(1, len(self.dense)))()
-        for k, s in enumerate(self.dense):
-            self.pieces[k] = _lib.Piece(None, s.offset, s.numel)
+        self.slots = [s for s in slots if s.numel]
+        self.pieces = (_lib.Piece * max(1, len(self.slots)))()
+        for k, s in enumerate(self.slots):
+            self.pieces[k] = _lib.Piece(None, s.offset, s.numel, 0 if s.dense else 1, 0)
+        self.n = len(self.slots)
         self.masters = ()
-        self.idx, self.e = ctx.raw_index(layer, world, stride, device)
+        self.base = None
         self.key = _lib.Key(ctx.root_seed, 0, layer, 0, 0)
         self.keyp = ctypes.byref(self.key)
         # the reference's ledger records of this collective (sharded.py:349-371, 403-429)
         probe = LedgerEntry(step=0)
-        for s in self.dense:
+        for s in self.slots:
+            if not s.dense:
+                continue
             if kind == "allgather":
                 record_allgather(probe, f"group{layer}.{s.name}", [(0, s.numel)] * world, ctx.wspec)
             else:
@@ -205,6 +198,7 @@ class QSDPAllGather(AllGather):
     def __call__(self, output_tensor, input_tensor, group, async_op=False):
         from . import _lib
         from .quantize import _DTYPE_CODE
+        t0 = time.perf_counter()
         c = self.ctx
         if output_tensor.dtype not in (torch.float32, torch.bfloat16):
             raise ValueError("QSDP all-gather writes fp32 or bf16 parameters")
@@ -213,32 +207,33 @@ class QSDPAllGather(AllGather):
         pl = self.plans.get((world, n_in))
         if pl is None:
             pl = self.plans[(world, n_in)] = _LayerPlan(c, self.layer, world, n_in, output_tensor.device, "allgather")
-        masters = tuple(s.fsdp_param._sharded_param_data for s in pl.dense)  # fp32 master shards
-        if masters != pl.masters:
+        masters = [s.fsdp_param._sharded_param_data for s in pl.slots]  # fp32 master shards
+        ptrs = tuple(m.data_ptr() for m in masters)
+        if ptrs != pl.masters:
             for k, m in enumerate(masters):
-                if m.dtype != torch.float32 or m.numel() != pl.dense[k].numel:
+                if m.dtype != torch.float32 or m.numel() != pl.slots[k].numel:
                     raise ValueError("QSDP all-gather expects fp32 sharded parameters")
-                pl.pieces[k].src = m.data_ptr()
-            pl.masters = masters
-        if pl.dense:
-            if c.wspec.inner != "levels":  # the group's dense weights: one quantize, barrier, dequant
-                pl.key.step, pl.key.phase = c.step, c.phase
-                _lib.check(_lib.lib().qsdp_all_gather_pieces(
-                    c.ag._h, pl.pieces, len(pl.dense), _lib.F32, n_in, pl.keyp, output_tensor.data_ptr(),
-                    _DTYPE_CODE[output_tensor.dtype], torch.cuda.current_stream().cuda_stream))
-            else:  # learned levels: one collective per weight
-                key = SegmentKey(c.root_seed, c.step, self.layer, c.phase, 0)
-                for m, s in zip(masters, pl.dense):
+                pl.pieces[k].src = ptrs[k]
+            pl.masters = ptrs
+        if not pl.n:
+            pass
+        elif c.wspec.inner != "levels":  # the whole group: one quantize, one barrier, one dequant
+            pl.key.step, pl.key.phase = c.step, c.phase
+            _lib.check(_lib.lib().qsdp_all_gather_pieces(
+                c.ag._h, pl.pieces, pl.n, _lib.F32, n_in, pl.keyp, output_tensor.data_ptr(),
+                _DTYPE_CODE[output_tensor.dtype], torch.cuda.current_stream().cuda_stream))
+        else:  # learned levels: one collective per weight, full-precision pieces in one more
+            key = SegmentKey(c.root_seed, c.step, self.layer, c.phase, 0)
+            raw = [(m, s.offset, s.numel, True) for m, s in zip(masters, pl.slots) if not s.dense]
+            for m, s in zip(masters, pl.slots):
+                if s.dense:
                     c.ag.all_gather(m, [(q * n_in + s.offset, s.numel) for q in range(world)], key,
                                     output_tensor[s.offset:])
-        if pl.e:  # full precision: what FSDP2 itself would gather for these parameters
-            send = input_tensor.index_select(0, pl.idx[:pl.e])
-            recv = torch.empty(world * pl.e, dtype=input_tensor.dtype, device=input_tensor.device)
-            dist.all_gather_into_tensor(recv, send, group=group)
-            output_tensor.index_copy_(0, pl.idx, recv)
-            c.calls["raw_allgather"] += 1
+            if raw:
+                c.ag.all_gather_pieces(raw, n_in, key, output_tensor)
         c.record(pl.ledger)
         c.calls["allgather"] += 1
+        c.host_s["allgather"] += time.perf_counter() - t0
         return None
 
 
@@ -256,6 +251,7 @@ class QSDPReduceScatter(ReduceScatter):
 
     def __call__(self, output_tensor, input_tensor, group, op, async_op=False):
         from . import _lib
+        t0 = time.perf_counter()
         if op not in (dist.ReduceOp.AVG,) and getattr(op, "op", op) != dist.ReduceOp.AVG:
             raise ValueError("QSDP reduce-scatter computes the average (ReduceOp.AVG)")
         if input_tensor.dtype != torch.float32 or output_tensor.dtype != torch.float32:
@@ -267,22 +263,19 @@ class QSDPReduceScatter(ReduceScatter):
         if pl is None:
             pl = self.plans[(world, n_out)] = _LayerPlan(c, self.layer, world, n_out, output_tensor.device,
                                                          "reducescatter")
-        if pl.dense:
-            base = input_tensor.data_ptr()
-            for k, s in enumerate(pl.dense):
+        base = input_tensor.data_ptr()
+        if base != pl.base:
+            for k, s in enumerate(pl.slots):
                 pl.pieces[k].src = base + 4 * s.offset
-            pl.key.step, pl.key.phase, pl.key.worker = c.step, PHASE_GRAD, c.rank
+            pl.base = base
+        pl.key.step, pl.key.phase, pl.key.worker = c.step, PHASE_GRAD, c.rank
+        if pl.n:
             _lib.check(_lib.lib().qsdp_reduce_scatter_pieces(
-                c.rs._h, pl.pieces, len(pl.dense), _lib.F32, n_out, pl.keyp, output_tensor.data_ptr(), _lib.F32,
+                c.rs._h, pl.pieces, pl.n, _lib.F32, n_out, pl.keyp, output_tensor.data_ptr(), _lib.F32,
                 torch.cuda.current_stream().cuda_stream))
-        if pl.e:
-            send = input_tensor.index_select(0, pl.idx)
-            recv = torch.empty(pl.e, dtype=input_tensor.dtype, device=input_tensor.device)
-            dist.reduce_scatter_tensor(recv, send, op=dist.ReduceOp.AVG, group=group)
-            output_tensor.index_copy_(0, pl.idx[:pl.e], recv)
-            c.calls["raw_reducescatter"] += 1
         c.record(pl.ledger)
         c.calls["reducescatter"] += 1
+        c.host_s["reducescatter"] += time.perf_counter() - t0
         return None
 
 

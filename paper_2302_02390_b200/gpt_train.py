@@ -62,9 +62,13 @@ def shard_model(model, mode: str, wspec: QuantSpec | None = None, gspec: QuantSp
     # largest group (codes padded per piece to 16 B, meta per piece to whole buckets)
     bucket = max((wspec or QuantSpec(8, 1024, "shift")).bucket, (gspec or QuantSpec(8, 1024)).bucket)
 
-    def group_need(params):
+    min_bits = min((wspec or QuantSpec(8, 1024, "shift")).bits, (gspec or QuantSpec(8, 1024)).bits)
+
+    def group_need(params):  # slot elements: quantized pieces + the full-precision ones' fp32 bytes
         dense = [p for p in params if p.dim() >= 2]
-        return _shard_numel(dense, world) + len(dense) * (bucket + 16)
+        raw = [p for p in params if p.dim() < 2]
+        return (_shard_numel(dense, world) + len(dense) * (bucket + 16) +
+                (_shard_numel(raw, world) + 4 * len(raw)) * 32 // min_bits)
     inner_ids = {id(p) for b in blocks for p in b.parameters()}
     max_shard = max([group_need(list(b.parameters())) for b in blocks] +
                     [group_need([p for p in model.parameters() if id(p) not in inner_ids])])

@@ -62,6 +62,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--modes", default="fsdp,qsdp")
     ap.add_argument("--out", default="")
+    ap.add_argument("--cprofile", action="store_true", help="rank 0: cProfile 2 more steps per mode (host hot spots)")
     ap.add_argument("--trace", default="", help="rank 0: torch.profiler chrome trace of 2 more steps per mode "
                                                 "(file prefix)")
     a = ap.parse_args()
@@ -85,7 +86,9 @@ def main():
         res[mode] = {"ms_per_step": round(med, 2), "steps_per_s": round(1e3 / med, 3),
                      "tokens_per_s": round(world * a.batch * a.seq / (med * 1e-3), 1),
                      "loss_first_last": [round(losses[0], 4), round(losses[-1], 4)],
-                     "calls": ctx.calls if ctx is not None else None}
+                     "calls": ctx.calls if ctx is not None else None,
+                     "host_ms_per_step_in_comm_hooks": ({k: round(1e3 * v / (a.steps + a.warmup), 3)
+                                                         for k, v in ctx.host_s.items()} if ctx is not None else None)}
         res["params"] = nparam
         if a.trace and rank == 0:
             from torch.profiler import ProfilerActivity, profile
@@ -94,6 +97,16 @@ def main():
             prof.export_chrome_trace(f"{a.trace}_{mode}.json")
         elif a.trace:
             run_training(model, ctx, steps=2, batch=a.batch, seq=a.seq, warmup=0)
+        if a.cprofile:
+            import cProfile
+            import pstats
+            pr = cProfile.Profile()
+            pr.enable()
+            run_training(model, ctx, steps=2, batch=a.batch, seq=a.seq, warmup=0)
+            pr.disable()
+            if rank == 0:
+                print(f"== cProfile {mode} (2 steps)", flush=True)
+                pstats.Stats(pr).sort_stats("tottime").print_stats(25)
         if ctx is not None:
             ctx.close()
         del model

@@ -309,22 +309,31 @@ def philox_collectives(rank, world, dev):
 
 def group_pieces(rank, world, dev):
     """qsdp_all_gather_pieces / qsdp_reduce_scatter_pieces: several equal-per-rank pieces at
-    fixed offsets of a rank's flat buffer (an FSDP2 group), keyed start = q*stride + offset."""
+    fixed offsets of a rank's flat buffer (an FSDP2 group), keyed start = q*stride + offset;
+    the gaps between them are full-precision pieces (``raw``: biases / norms, sharded.py:
+    359-371, 414-429) carried by the same call -- all-gather: the values cast to the output
+    dtype, reduce-scatter: (0.0 + v_0 + ... + v_{P-1}) / P in fp64, rounded once."""
     fails = 0
     rng = np.random.default_rng(23)
     sizes = [5000, 1024 * 7, 333, 4096 * 3 + 8]
-    offs, off = [], 0
-    for n in sizes:
+    raw_sizes = [5, 3000, 1, 7]  # after each quantized piece
+    offs, roffs, off = [], [], 0
+    for n, r in zip(sizes, raw_sizes):
         offs.append(off)
-        off += n + 5  # gaps: full-precision parameters of the group live there
+        off += n
+        roffs.append(off)
+        off += r
     stride = off
-    cap = sum(sizes) + len(sizes) * (1024 + 16)
+    cap = sum(sizes) + len(sizes) * (1024 + 16) + 4 * (sum(raw_sizes) + 4 * len(raw_sizes))
     comm = QSDPComm(cap, QuantSpec(8, 1024, "shift"), QuantSpec(8, 1024, "uniform_stochastic"))
     shards = [[(rng.standard_normal(n) * 0.02).astype(np.float32) for n in sizes] for _ in range(world)]
+    rshards = [[(rng.standard_normal(n) * 0.5).astype(np.float32) for n in raw_sizes] for _ in range(world)]
     grads = [(rng.standard_normal(world * stride) * 1e-3).astype(np.float32) for _ in range(world)]
     for out_dt in (torch.float32, torch.bfloat16):
         out = torch.zeros(world * stride, dtype=out_dt, device=dev)
         pieces = [(torch.from_numpy(shards[rank][k]).to(dev), offs[k], sizes[k]) for k in range(len(sizes))]
+        pieces += [(torch.from_numpy(rshards[rank][k]).to(dev), roffs[k], raw_sizes[k], True)
+                   for k in range(len(raw_sizes))]
         comm.all_gather_pieces(pieces, stride, SegmentKey(2, 3, 4, 1, 0), out)
         got = out.float().cpu().numpy()
         for q in range(world):
@@ -335,8 +344,15 @@ def group_pieces(rank, world, dev):
                 if not np.array_equal(got[a:a + n], exp.to(out_dt).float().numpy()):
                     fails += 1
                     print(f"rank {rank} pieces AG {out_dt} q {q} k {k}: mismatch", flush=True)
+            for k, n in enumerate(raw_sizes):
+                a = q * stride + roffs[k]
+                exp = torch.from_numpy(rshards[q][k]).to(out_dt).float().numpy()
+                if not np.array_equal(got[a:a + n], exp):
+                    fails += 1
+                    print(f"rank {rank} pieces AG raw {out_dt} q {q} k {k}: mismatch", flush=True)
     rs = torch.zeros(stride, device=dev)
-    comm.reduce_scatter_pieces(torch.from_numpy(grads[rank]).to(dev), list(zip(offs, sizes)), stride,
+    rs_pieces = list(zip(offs, sizes)) + [(o, n, True) for o, n in zip(roffs, raw_sizes)]
+    comm.reduce_scatter_pieces(torch.from_numpy(grads[rank]).to(dev), rs_pieces, stride,
                                SegmentKey(2, 3, 4, 2, rank), rs)
     got = rs.cpu().numpy()
     for k, n in enumerate(sizes):
@@ -348,6 +364,14 @@ def group_pieces(rank, world, dev):
         if not np.array_equal(got[offs[k]:offs[k] + n], (acc / world).astype(np.float32)):
             fails += 1
             print(f"rank {rank} pieces RS k {k}: mismatch", flush=True)
+    for k, n in enumerate(raw_sizes):
+        a = rank * stride + roffs[k]
+        acc = np.zeros(n)
+        for p in range(world):
+            acc = acc + grads[p][a:a + n].astype(np.float64)
+        if not np.array_equal(got[roffs[k]:roffs[k] + n], (acc / world).astype(np.float32)):
+            fails += 1
+            print(f"rank {rank} pieces RS raw k {k}: mismatch", flush=True)
     comm.close()
     return fails
 

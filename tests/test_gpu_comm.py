@@ -141,16 +141,23 @@ def test_group_pieces_world1(oracle):
         for n in sizes:
             offs.append(off)
             off += n + gap
-        comm = QSDPComm(sum(sizes) + len(sizes) * 1040, QuantSpec(8, 1024, "shift"),
+        comm = QSDPComm(sum(sizes) + len(sizes) * 1040 + 8 * (gap + 4) * len(sizes), QuantSpec(8, 1024, "shift"),
                         QuantSpec(4, 1024, "uniform_stochastic"), device=dev)
         xs = [(rng.standard_normal(n) * 0.02).astype(np.float32) for n in sizes]
         out = torch.zeros(off, device=dev)
-        comm.all_gather_pieces([(torch.from_numpy(x).to(dev), o, n) for x, o, n in zip(xs, offs, sizes)], off,
+        base = torch.from_numpy((rng.standard_normal(off) * 0.3).astype(np.float32)).to(dev)
+        raw = [(base[o + n:o + n + gap], o + n, gap, True) for o, n in zip(offs, sizes) if gap]  # full precision
+        comm.all_gather_pieces([(torch.from_numpy(x).to(dev), o, n) for x, o, n in zip(xs, offs, sizes)] + raw, off,
                                SegmentKey(1, 2, 3, 0, 0), out)
         g = (rng.standard_normal(off) * 1e-3).astype(np.float32)
         rs = torch.zeros(off, device=dev)
-        comm.reduce_scatter_pieces(torch.from_numpy(g).to(dev), list(zip(offs, sizes)), off, SegmentKey(1, 2, 3, 2, 0), rs)
+        comm.reduce_scatter_pieces(torch.from_numpy(g).to(dev),
+                                   list(zip(offs, sizes)) + [(o, n, True) for _, o, n, _ in raw], off,
+                                   SegmentKey(1, 2, 3, 2, 0), rs)
         o, r = out.cpu().numpy(), rs.cpu().numpy()
+        for _, a, n, _ in raw:  # full-precision pieces: copied / averaged over one rank
+            assert np.array_equal(o[a:a + n], base[a:a + n].cpu().numpy())
+            assert np.array_equal(r[a:a + n], g[a:a + n])
         for x, a, n in zip(xs, offs, sizes):
             c, m, _ = oracle.quantize_segment(x, a, 1024, 8, 0, (1, 2, 3, 0, 0), 8)
             assert np.array_equal(o[a:a + n], oracle.dequantize_segment(c, m, n, 1024, 8, 8).astype(np.float32))
