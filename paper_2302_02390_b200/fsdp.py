@@ -104,7 +104,9 @@ class QSDPContext:
         self.step = 0
         self.phase = PHASE_W_FWD
         self.calls = {"allgather": 0, "reducescatter": 0}
-        self.host_s = {"allgather": 0.0, "reducescatter": 0.0}  # host time inside the comm hooks
+        # host time inside the comm hooks (and inside their C-ABI calls)
+        self.host_s = {"allgather": 0.0, "reducescatter": 0.0, "allgather_capi": 0.0, "reducescatter_capi": 0.0}
+        self.capi_samples: list[float] = []  # per-call host time of the all-gather C-ABI call
         self.layouts: dict[int, list[ParamSlot]] = {}
         self.param_bits = None  # width of the full-precision all-gather (set from the param dtype)
         # the reference's per-step communication ledger (sharded.py:115-181)
@@ -219,9 +221,14 @@ class QSDPAllGather(AllGather):
             pass
         elif c.wspec.inner != "levels":  # the whole group: one quantize, one barrier, one dequant
             pl.key.step, pl.key.phase = c.step, c.phase
-            _lib.check(_lib.lib().qsdp_all_gather_pieces(
-                c.ag._h, pl.pieces, pl.n, _lib.F32, n_in, pl.keyp, output_tensor.data_ptr(),
-                _DTYPE_CODE[output_tensor.dtype], torch.cuda.current_stream().cuda_stream))
+            stream, optr, odt = torch.cuda.current_stream().cuda_stream, output_tensor.data_ptr(), _DTYPE_CODE[output_tensor.dtype]
+            t1 = time.perf_counter()
+            rc = _lib.hot().qsdp_all_gather_pieces(c.ag._h, pl.pieces, pl.n, _lib.F32, n_in, pl.keyp, optr, odt, stream)
+            dt = time.perf_counter() - t1
+            c.host_s["allgather_capi"] += dt
+            if len(c.capi_samples) < 4096:
+                c.capi_samples.append(dt)
+            _lib.check(rc)
         else:  # learned levels: one collective per weight, full-precision pieces in one more
             key = SegmentKey(c.root_seed, c.step, self.layer, c.phase, 0)
             raw = [(m, s.offset, s.numel, True) for m, s in zip(masters, pl.slots) if not s.dense]
@@ -270,9 +277,12 @@ class QSDPReduceScatter(ReduceScatter):
             pl.base = base
         pl.key.step, pl.key.phase, pl.key.worker = c.step, PHASE_GRAD, c.rank
         if pl.n:
-            _lib.check(_lib.lib().qsdp_reduce_scatter_pieces(
-                c.rs._h, pl.pieces, pl.n, _lib.F32, n_out, pl.keyp, output_tensor.data_ptr(), _lib.F32,
-                torch.cuda.current_stream().cuda_stream))
+            stream, optr = torch.cuda.current_stream().cuda_stream, output_tensor.data_ptr()
+            t1 = time.perf_counter()
+            rc = _lib.hot().qsdp_reduce_scatter_pieces(c.rs._h, pl.pieces, pl.n, _lib.F32, n_out, pl.keyp, optr,
+                                                       _lib.F32, stream)
+            c.host_s["reducescatter_capi"] += time.perf_counter() - t1
+            _lib.check(rc)
         c.record(pl.ledger)
         c.calls["reducescatter"] += 1
         c.host_s["reducescatter"] += time.perf_counter() - t0

@@ -89,6 +89,12 @@ def main():
                      "calls": ctx.calls if ctx is not None else None,
                      "host_ms_per_step_in_comm_hooks": ({k: round(1e3 * v / (a.steps + a.warmup), 3)
                                                          for k, v in ctx.host_s.items()} if ctx is not None else None)}
+        if ctx is not None and ctx.capi_samples:
+            import numpy as np
+            v = np.array(ctx.capi_samples) * 1e6
+            res[mode]["allgather_capi_us"] = {"median": round(float(np.median(v)), 1),
+                                              "p90": round(float(np.percentile(v, 90)), 1),
+                                              "max": round(float(v.max()), 1), "n": int(v.size)}
         res["params"] = nparam
         if a.trace and rank == 0:
             from torch.profiler import ProfilerActivity, profile
