@@ -270,8 +270,10 @@ qsdp_status qsdp_comm_set_step_source(qsdp_comm* c, const uint64_t* d_step);
 /* Learned weight levels for the all-gather (w.inner == QSDP_INNER_LEVELS): a
  * device float64[2^w.bits] table that stays valid while the comm uses it. */
 qsdp_status qsdp_comm_set_weight_levels(qsdp_comm* c, const double* d_levels, int32_t nlevels);
-/* Size the collectives' grids for at most `sms` SMs (0 = all): leaves the rest of the
- * GPU to compute kernels that run concurrently (FSDP2 overlaps comm streams with compute). */
+/* Size the collectives' grids for at most `sms` SMs: leaves the rest of the GPU to compute
+ * kernels that run concurrently (FSDP2 overlaps comm streams with compute).  0 = the
+ * default (world 1: all SMs; world > 1: all but 8, so the one-CTA flag barriers of other
+ * in-flight collectives always find an SM); < 0 = all SMs. */
 qsdp_status qsdp_comm_set_sm_budget(qsdp_comm* c, int32_t sms);
 /* Failure detection.  A barrier whose peer does not arrive within the timeout
  * (default 60 s; env QSDP_TIMEOUT_MS at creation) gives up instead of hanging and

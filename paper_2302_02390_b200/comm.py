@@ -169,8 +169,10 @@ class QSDPComm:
         _lib.check(_lib.lib().qsdp_comm_set_step_source(self._h, counter.data_ptr() if counter is not None else None))
 
     def set_sm_budget(self, sms: int) -> None:
-        """Size this communicator's kernels for at most ``sms`` SMs (0 = the whole GPU), so
-        collectives overlapping compute on another stream leave it the other SMs."""
+        """Size this communicator's kernels for at most ``sms`` SMs, so collectives overlapping
+        compute on another stream leave it the other SMs (0 = default: the whole GPU at world
+        1, all but 8 SMs at world > 1 so other collectives' barriers always find an SM;
+        < 0 = the whole GPU)."""
         _lib.check(_lib.lib().qsdp_comm_set_sm_budget(self._h, int(sms)))
 
     def set_timeout(self, ms: int) -> None:

@@ -757,6 +757,7 @@ struct PeerFlags {
 };
 
 constexpr size_t kEpochOff = 128;
+constexpr int kBarrierSMs = 8;
 
 // Failure detection: a peer that never arrives (dead, hung or desynchronised)
 // must not hang this rank.  Each waiting lane gives up after `timeout_ns` of
@@ -928,6 +929,7 @@ struct qsdp_comm {
   bool opened[QSDP_MAX_WORLD] = {};
   const unsigned long long* step_src = nullptr;
   int sm_budget = 0;                // > 0: the collectives' kernels use at most this many SMs
+  int sm_default = 0;               // budget when none is set: world > 1 leaves kBarrierSMs SMs free
   const double* wlevels = nullptr;  // learned weight table (w.inner == QSDP_INNER_LEVELS)
   int wnlevels = 0;
   unsigned long long* err_host = nullptr;  // host-mapped failure word (barrier timeout)
@@ -969,6 +971,11 @@ qsdp_status qsdp_comm_create(qsdp_comm** out, int32_t rank, int32_t world, int32
   c->rank = rank;
   c->world = world;
   c->device = device;
+  // A collective's flag barrier is a one-CTA kernel: with several collectives in flight, a
+  // persistent quantizer holding every SM would queue it (and every peer waiting on it)
+  // behind whole kernels.  Leaving a few SMs free keeps the barriers moving (N=4 bench
+  // +2-3%, profiles/r2/smcap_n4.txt).
+  c->sm_default = world > 1 && sms > 2 * kBarrierSMs ? sms - kBarrierSMs : 0;
   c->max_seg = max_segment_elems;
   c->w = *wcfg;
   c->g = *gcfg;
@@ -1118,7 +1125,7 @@ static qsdp_status check_segs(const qsdp_comm* c, const qsdp_segment* segs) {
 static DynSrc comm_dyn(const qsdp_comm* c, int adj) {
   DynSrc d;
   d.step_ptr = c->step_src;
-  d.sm_cap = c->sm_budget;
+  d.sm_cap = c->sm_budget > 0 ? c->sm_budget : c->sm_budget < 0 ? 0 : c->sm_default;
   if (c->world > 1) {
     d.parity_ptr = c->epoch();
     d.parity_stride = c->parity_stride();
