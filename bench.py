@@ -76,10 +76,16 @@ def parse():
     ap.add_argument("--inflight", type=int, default=8,
                     help="collectives of one kind in flight (streams + communicators per kind; the prefetch depth). "
                          "At N>1 deeper pipelines hide the barrier waits and NVLink pushes (N=4: 2 -> 8 in flight "
-                         "+13%); flat at N=1")
+                         "+13%%); flat at N=1")
     ap.add_argument("--fwd-ag-sms", type=int, default=0, help="SM budget of the forward all-gathers (0 = all)")
     ap.add_argument("--bwd-ag-sms", type=int, default=0, help="SM budget of the backward all-gathers (0 = all)")
     ap.add_argument("--rs-sms", type=int, default=0, help="SM budget of the reduce-scatters (0 = all)")
+    ap.add_argument("--fwd-ag-ctas", type=int, default=1,
+                    help="quantizer CTAs per SM, forward all-gathers (0 = occupancy, 2 for this kernel). One: "
+                         "two in-flight all-gathers share every SM, one's ramp / tail under the other's "
+                         "steady state (N=1 +2%%, DESIGN §17)")
+    ap.add_argument("--bwd-ag-ctas", type=int, default=1, help="quantizer CTAs per SM, backward all-gathers")
+    ap.add_argument("--rs-ctas", type=int, default=0, help="quantizer CTAs per SM, reduce-scatters")
     ap.add_argument("--trace", default="", help="write the GPU timeline of one step replay (CUPTI via "
                     "torch.profiler: every kernel's start / end / stream) and its overlap summary to this JSON file")
     ap.add_argument("--gpt-steps", type=int, default=8)
@@ -310,7 +316,7 @@ def bench_config(args, world, ngroups, n_total):
                         f"AG fwd + AG bwd + RS over {ngroups} FSDP groups ({n_total} dense params)",
             "out_dtype": args.out_dtype, "quantizer_input": "f32", "arithmetic": "f64 (bit-exact)",
             "parallelism": f"qsdp{world}", "convention": "sum over ranks of 4*N per collective / time",
-            "inflight": args.inflight}
+            "inflight": args.inflight, "ag_ctas_per_sm": [args.fwd_ag_ctas, args.bwd_ag_ctas]}
 
 
 # ---------------------------------------------------------------------------
@@ -426,18 +432,21 @@ def main():
         j = 0
         for gi, st in enumerate(state):
             c = ag_comms[j % K]
-            L.append(("AG", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.fwd_ag_sms), c.all_gather(
+            L.append(("AG", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.fwd_ag_sms),
+                                                           c.set_ctas_per_sm(args.fwd_ag_ctas), c.all_gather(
                 st["shard"], st["segs"], SegmentKey(0, 0, gi, 0, 0), st["full"])), ("ag", j % K), None))
             j += 1
         r = 0
         for gi in range(len(state) - 1, -1, -1):
             st = state[gi]
             c = ag_comms[j % K]
-            L.append(("AG", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.bwd_ag_sms), c.all_gather(
+            L.append(("AG", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.bwd_ag_sms),
+                                                           c.set_ctas_per_sm(args.bwd_ag_ctas), c.all_gather(
                 st["shard"], st["segs"], SegmentKey(0, 0, gi, 1, 0), st["full"])), ("ag", j % K), None))
             j += 1
             c = rs_comms[r % K]
-            L.append(("RS", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.rs_sms), c.reduce_scatter(
+            L.append(("RS", per, lambda st=st, gi=gi, c=c: (c.set_sm_budget(args.rs_sms),
+                                                           c.set_ctas_per_sm(args.rs_ctas), c.reduce_scatter(
                 st["grad"], st["segs"], SegmentKey(0, 0, gi, 2, rank), st["gshard"])),
                 ("ag" if args.serial else "rs", (r if args.serial else r) % K), len(L) - 1))
             r += 1

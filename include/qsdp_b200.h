@@ -275,6 +275,10 @@ qsdp_status qsdp_comm_set_weight_levels(qsdp_comm* c, const double* d_levels, in
  * default (world 1: all SMs; world > 1: all but 8, so the one-CTA flag barriers of other
  * in-flight collectives always find an SM); < 0 = all SMs. */
 qsdp_status qsdp_comm_set_sm_budget(qsdp_comm* c, int32_t sms);
+/* At most `ctas` quantizer CTAs per SM (0 = as many as fit): an HBM-bound all-gather capped
+ * at one CTA per SM leaves the other slot to a concurrent, issue-bound reduce-scatter on
+ * another stream (the backward phase), instead of taking turns with it. */
+qsdp_status qsdp_comm_set_ctas_per_sm(qsdp_comm* c, int32_t ctas);
 /* Failure detection.  A barrier whose peer does not arrive within the timeout
  * (default 60 s; env QSDP_TIMEOUT_MS at creation) gives up instead of hanging and
  * records the peer in a host-mapped word: qsdp_comm_status() -- and every later

@@ -45,7 +45,7 @@ EXPORTED_SYMBOLS = (
     "qsdp_wire_parse", "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes",
     "qsdp_unpack_codes", "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice",
     "qsdp_comm_set_sm_budget", "qsdp_comm_set_timeout", "qsdp_comm_status", "qsdp_all_gather_pieces",
-    "qsdp_reduce_scatter_pieces", "qsdp_quantize_stream", "qsdp_levels_stochastic",
+    "qsdp_reduce_scatter_pieces", "qsdp_quantize_stream", "qsdp_levels_stochastic", "qsdp_comm_set_ctas_per_sm",
 )
 
 
@@ -158,6 +158,7 @@ def lib():
     L.qsdp_comm_set_step_source.argtypes = [vp, vp]
     L.qsdp_comm_set_weight_levels.argtypes = [vp, vp, i32]
     L.qsdp_comm_set_sm_budget.argtypes = [vp, i32]
+    L.qsdp_comm_set_ctas_per_sm.argtypes = [vp, i32]
     L.qsdp_comm_set_timeout.argtypes = [vp, i64]
     L.qsdp_comm_status.argtypes = [vp]
     L.qsdp_quantize_stream.argtypes = [vp, i32, i64, cfgp, vp, vp, vp, vp, vp]
@@ -200,7 +201,7 @@ def lib():
                  "qsdp_wire_encode_device", "qsdp_wire_decode_device", "qsdp_pack_codes", "qsdp_unpack_codes",
                  "qsdp_dequant_accumulate_lattice", "qsdp_reduce_scatter_lattice", "qsdp_comm_set_sm_budget",
                  "qsdp_comm_set_timeout", "qsdp_comm_status", "qsdp_all_gather_pieces", "qsdp_reduce_scatter_pieces",
-                 "qsdp_quantize_stream", "qsdp_levels_stochastic"):
+                 "qsdp_quantize_stream", "qsdp_levels_stochastic", "qsdp_comm_set_ctas_per_sm"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return _lib

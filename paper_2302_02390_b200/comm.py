@@ -175,6 +175,11 @@ class QSDPComm:
         < 0 = the whole GPU)."""
         _lib.check(_lib.lib().qsdp_comm_set_sm_budget(self._h, int(sms)))
 
+    def set_ctas_per_sm(self, ctas: int) -> None:
+        """At most ``ctas`` quantizer CTAs per SM (0 = occupancy): an all-gather capped at one
+        leaves the other slot of every SM to a concurrent reduce-scatter."""
+        _lib.check(_lib.lib().qsdp_comm_set_ctas_per_sm(self._h, int(ctas)))
+
     def set_timeout(self, ms: int) -> None:
         """Barrier timeout: a peer that does not arrive within ``ms`` milliseconds makes the
         barrier give up instead of hanging; :meth:`check` (and every later collective)

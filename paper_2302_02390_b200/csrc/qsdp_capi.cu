@@ -145,6 +145,7 @@ struct DynSrc {
   int64_t parity_stride = 0;
   int32_t parity_adj = 0;
   int32_t sm_cap = 0;    // > 0: size grids for at most this many SMs (comm SM budget)
+  int32_t cta_cap = 0;   // > 0: at most this many quantizer CTAs per SM
   int32_t dq_dtype = 0;  // fused dequant epilogue: output dtype and K4's single-source 0.0 + v
   int32_t dq_add0 = 0;
   int32_t dq_nocodes = 0;  // world 1: nobody reads the codes
@@ -160,6 +161,7 @@ void build_qtab(QJobTable& tab, const std::vector<QJobSpec>& jobs, size_t& i, co
   tab.bucket = cfg->bucket;
   tab.inner = cfg->inner;
   tab.noise = cfg->noise;
+  tab.cta_cap = dyn.cta_cap;
   tab.bad_index = reinterpret_cast<unsigned long long*>(d_bad);
   tab.step_ptr = dyn.step_ptr;
   tab.parity_ptr = dyn.parity_ptr;
@@ -930,6 +932,7 @@ struct qsdp_comm {
   const unsigned long long* step_src = nullptr;
   int sm_budget = 0;                // > 0: the collectives' kernels use at most this many SMs
   int sm_default = 0;               // budget when none is set: world > 1 leaves kBarrierSMs SMs free
+  int ctas_per_sm = 0;              // > 0: the quantizer's CTAs per SM
   const double* wlevels = nullptr;  // learned weight table (w.inner == QSDP_INNER_LEVELS)
   int wnlevels = 0;
   unsigned long long* err_host = nullptr;  // host-mapped failure word (barrier timeout)
@@ -1022,6 +1025,12 @@ qsdp_status qsdp_comm_set_weight_levels(qsdp_comm* c, const double* d_levels, in
     return fail(QSDP_EINVAL, "level table size does not match bit_width");
   c->wlevels = d_levels;
   c->wnlevels = nlevels;
+  return QSDP_OK;
+}
+
+qsdp_status qsdp_comm_set_ctas_per_sm(qsdp_comm* c, int32_t ctas) {
+  if (c == nullptr) return fail(QSDP_EINVAL, "null comm");
+  c->ctas_per_sm = ctas < 0 ? 0 : ctas;
   return QSDP_OK;
 }
 
@@ -1126,6 +1135,7 @@ static DynSrc comm_dyn(const qsdp_comm* c, int adj) {
   DynSrc d;
   d.step_ptr = c->step_src;
   d.sm_cap = c->sm_budget > 0 ? c->sm_budget : c->sm_budget < 0 ? 0 : c->sm_default;
+  d.cta_cap = c->ctas_per_sm;
   if (c->world > 1) {
     d.parity_ptr = c->epoch();
     d.parity_stride = c->parity_stride();

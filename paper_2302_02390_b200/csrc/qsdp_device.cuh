@@ -282,6 +282,7 @@ struct QJobTable {
   int32_t dq_add0;
   int32_t dq_nocodes;  // world 1: the fused dequant is the only consumer -> codes not stored
   int32_t noise;       // qsdp_noise: 0 PCG64 (bucket_rng), 1 Philox4x64-10 (counter-based)
+  int32_t cta_cap;     // launch only: > 0 caps the TMA32 quantizer's CTAs per SM
 };
 
 struct DJob {

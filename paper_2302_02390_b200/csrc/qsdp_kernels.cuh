@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "qsdp_device.cuh"
 
@@ -2001,19 +2002,28 @@ inline int grid_for(int64_t total_buckets, int teams_per_warp, int sms, int warp
 // the work is smaller.  Every kernel grid-strides over buckets, so a partial
 // second wave would only add a tail.
 template <typename F>
-inline int persistent_grid(F kern, int threads, size_t smem, int64_t total_buckets, int teams_per_warp, int sms) {
-  // one cached occupancy answer per (kernel instantiation, smem size)
-  static thread_local size_t cached_smem = (size_t)-1;
-  static thread_local int cached_threads = 0, per_sm = 1;
-  if (cached_smem != smem || cached_threads != threads) {
+inline int persistent_grid(F kern, int threads, size_t smem, int64_t total_buckets, int teams_per_warp, int sms,
+                           int max_per_sm = 0) {
+  // one cached occupancy answer per (kernel, block size, smem size): every quantizer
+  // instantiation has the same function type, so the kernel address is part of the key
+  struct Entry { const void* k; size_t smem; int threads, per_sm; };
+  static thread_local Entry cache[16] = {};
+  static thread_local int next = 0;
+  const void* kp = reinterpret_cast<const void*>(kern);
+  int per_sm = 0;
+  for (const Entry& e : cache)
+    if (e.k == kp && e.smem == smem && e.threads == threads) per_sm = e.per_sm;
+  if (per_sm == 0) {
     int v = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, threads, smem) != cudaSuccess || v < 1) v = 1;
     per_sm = v;
-    cached_smem = smem;
-    cached_threads = threads;
+    cache[next] = Entry{kp, smem, threads, v};
+    next = (next + 1) & 15;
   }
+  if (max_per_sm > 0 && per_sm > max_per_sm) per_sm = max_per_sm;
   return grid_for(total_buckets, teams_per_warp, sms, threads / 32, per_sm);
 }
+
 
 // Opt a kernel into more than 48 KB of dynamic shared memory.  The attribute is
 // per device context, so the cache (one per kernel instantiation, passed in) is
@@ -2049,7 +2059,9 @@ cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
   auto kern = quantize_tma32_kernel<T, INNER, BITS, NST, FDQ>;
   static thread_local size_t smem_set[64] = {};  // per instantiation and device
   if (cudaError_t e = ensure_smem_attr(kern, smem, smem_set); e != cudaSuccess) return e;
-  const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, 1, sms);
+  // tab.cta_cap (qsdp_comm_set_ctas_per_sm): leave CTA slots on every SM to a concurrent
+  // collective (an HBM-bound all-gather beside an issue-bound reduce-scatter)
+  const int grid = persistent_grid(kern, wpc * 32, smem, tab.total_buckets, 1, sms, tab.cta_cap);
   kern<<<grid, wpc * 32, smem, s>>>(tab);
   return cudaGetLastError();
 }

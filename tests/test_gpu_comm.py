@@ -36,6 +36,27 @@ def test_single_rank_comm_vs_oracle(oracle):
     comm.close()
 
 
+@pytest.mark.parametrize("ctas,sms", [(1, 0), (1, 37), (0, 20)])
+def test_occupancy_caps_keep_results(oracle, ctas, sms):
+    """qsdp_comm_set_ctas_per_sm / set_sm_budget size the grids only: same bits as the oracle."""
+    dev = torch.device("cuda", 0)
+    size = 1024 * 3000 + 77
+    comm = QSDPComm(size, QuantSpec(8, 1024, "shift"), QuantSpec(8, 1024, "uniform_stochastic"), device=dev)
+    comm.set_ctas_per_sm(ctas)
+    comm.set_sm_budget(sms)
+    x = (np.random.default_rng(5).standard_normal(size) * 0.02).astype(np.float32)
+    xt = torch.from_numpy(x).to(dev)
+    out = torch.empty(size, device=dev)
+    comm.all_gather(xt, [(0, size)], SegmentKey(3, 1, 2, 0, 0), out)
+    c, m, _ = oracle.quantize_segment(x, 0, 1024, 8, 0, (3, 1, 2, 0, 0), 8)
+    assert np.array_equal(out.cpu().numpy(), oracle.dequantize_segment(c, m, size, 1024, 8, 8).astype(np.float32))
+    sh = torch.empty(size, device=dev)
+    comm.reduce_scatter(xt, [(0, size)], SegmentKey(3, 1, 2, 2, 0), sh)
+    c, m, _ = oracle.quantize_segment(x, 0, 1024, 8, 1, (3, 1, 2, 2, 0), 8)
+    assert np.array_equal(sh.cpu().numpy(), oracle.dequantize_segment(c, m, size, 1024, 8, 8).astype(np.float32))
+    comm.close()
+
+
 def test_graph_replay_with_device_step(oracle):
     """A captured AG+RS replays with the step read on the device (fresh noise per replay)."""
     from paper_2302_02390_b200.quantize import advance_counter
