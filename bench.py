@@ -588,6 +588,10 @@ def main():
         # the batch API) stay listed as kernels_unfused.
         osz = 4 if out_dt == torch.float32 else 2
         fused_kinds = {}
+        # the kernels' own throughput: serial on one stream, at full occupancy (the step pairs its
+        # in-flight all-gathers at --*-ag-ctas CTAs per SM; that schedule is timed separately below)
+        sched = (args.fwd_ag_ctas, args.bwd_ag_ctas, args.rs_ctas)
+        args.fwd_ag_ctas = args.bwd_ag_ctas = args.rs_ctas = 0
         for kind, sel in (("AG_K1_fused_dequant", "AG"), ("RS_K2_fused_dequant", "RS")):
             fns = [x[2] for x in launches if x[0] == sel]  # serial on one stream: the kernels' own throughput
             gk = capture(lambda fns=fns: [f() for f in fns], keep=True)
@@ -608,6 +612,17 @@ def main():
                                  "share_of_step": round(tk / ms_step, 4), "bytes_per_step": nb,
                                  "bytes_per_element": f"4 in + {osz if sel == 'AG' else 4} out + 12/{args.bucket} meta "
                                                       "(no codes: world 1 has no reader)"}
+        args.fwd_ag_ctas, args.bwd_ag_ctas, args.rs_ctas = sched
+        if fused_kinds and any(sched):  # the same serial graphs at the step's CTA caps
+            for kind, sel in (("AG_K1_fused_dequant", "AG"), ("RS_K2_fused_dequant", "RS")):
+                fns = [x[2] for x in launches if x[0] == sel]
+                gk = capture(lambda fns=fns: [f() for f in fns], keep=True)
+                gk.replay()
+                torch.cuda.synchronize(dev)
+                evk = time_graph(gk, args.steps)
+                torch.cuda.synchronize(dev)
+                tk = sum(a.elapsed_time(b) for a, b in evk) / args.steps
+                fused_kinds[kind]["gbs_at_step_ctas"] = round(fused_kinds[kind]["bytes_per_step"] / (tk * 1e-3) / 1e9, 1)
         kernels_unfused = None
         if fused_kinds:
             kernels_unfused, kernels = kernels, fused_kinds
@@ -623,11 +638,14 @@ def main():
                     "frac": round(ach / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
                     "bytes_per_launch": round(kernels[dom]["bytes_per_step"] / kernels[dom]["launches_per_step"]),
                     "method": "algorithmic bytes / CUDA-event time of that kernel's launches (graph of one step's "
-                              "launches of the kind, L2 flushed between replays)",
+                              "launches of the kind, serial, full occupancy, L2 flushed between replays)",
                     "frac_by_kernel": {k: round(v["gbs"] / hbm_peak, 4) for k, v in kernels.items()}}
         if "K2" in dom:
             roofline["note"] = ("K2 is integer-issue bound: one exact 128-bit PCG64 step per element "
                                 "(numpy's bucket_rng stream, DESIGN.md section 5)")
+        if "gbs_at_step_ctas" in kernels[dom]:
+            roofline["frac_at_step_ctas"] = {k: round(v["gbs_at_step_ctas"] / hbm_peak, 4) for k, v in kernels.items()
+                                             if "gbs_at_step_ctas" in v}
         if kernels_unfused is not None:
             roofline["frac_by_kernel_unfused"] = {k: round(v["gbs"] / hbm_peak, 4) for k, v in kernels_unfused.items()}
 
