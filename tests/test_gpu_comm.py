@@ -125,7 +125,7 @@ def _torchrun(script, nproc, port, extra_env=None, timeout=900):
     return r.stdout
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_multi_process_comm_one_gpu(world):
     """The one-process-per-rank C1/C2 protocol with every rank on cuda:0 (gloo host
     plumbing): CUDA IPC workspaces of the other processes, the push mirror, the
