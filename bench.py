@@ -711,7 +711,7 @@ def main():
                                                        + 12 * num_buckets(st["g"].numel, args.bucket) for st in state)}
         philox = {"noise": "np.random.Generator(np.random.Philox(SeedSequence(key))): Philox4x64-10, counter-based "
                            "(one 10-round block per 4 draws); K1 on the TMA32 path (one draw per bucket), K2 on the "
-                           "team kernels with the counter-based Coder"}
+                           "TMA32 octet path (two blocks per lane-octet; team kernels for other bucket shapes)"}
         for name, fn in (("K1_quantize_shift_philox", pq_w), ("K2_quantize_stochastic_philox", pq_g)):
             fn()
             gk = capture(fn)

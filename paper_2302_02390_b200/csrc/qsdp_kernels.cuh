@@ -755,12 +755,12 @@ __device__ __forceinline__ FusedDq fused_dq(const QJobTable& tab, const QJob& J,
 // Partial / unaligned / degenerate bucket (one per segment at most on the hot
 // path): per-lane seeding and the Coder path; out of line to keep the fast
 // loop's register budget.  Returns the bucket's f32 shift.
-template <typename T, int INNER, int BITS, int FDQ = 0>
+template <typename T, int INNER, int BITS, int FDQ = 0, int PH = 0>
 static __device__ __forceinline__ float quantize_bucket_general(const SeedPrefix& seed, uint64_t start, const T* x, int n,
                                                              int gl, uint8_t* cbase, float lof, float hif,
                                                              bool degenerate, int lane, const QJobTable& tab,
                                                              const QJob& J, int64_t off) {
-  Coder<T, INNER> cd;
+  Coder<T, INNER, PH> cd;
   float shift_f = 0.0f;
   if (!degenerate) cd.setup(lof, hif, BITS, seed, start, lane, 32, shift_f, tab.noise);
   const FusedDq fq = fused_dq<FDQ>(tab, J, off, lof, hif, degenerate ? 0.0f : shift_f, BITS);
@@ -835,12 +835,34 @@ static __device__ __noinline__ uint64_t stoch_octet_exact(const T* v, U128 st, U
   return w;
 }
 
+// Rare path of the Philox octet loop: the 8 codes again, each element certified, the exact
+// chain on the draw where the bound is not met.
+template <typename T, int BITS>
+static __device__ __noinline__ uint64_t philox_octet_exact(const T* v, Philox4 b0, Philox4 b1, double lo, double span,
+                                                           double K1, double top) {
+  using Tr = InTraits<T>;
+  uint64_t w = 0;
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t draw = i < 4 ? b0.v[i] : b1.v[i - 4];
+    double a = __dsub_rn(Tr::to_d(v[i]), lo);
+    if constexpr (sizeof(T) == 8) a = fmin(fmax(a, 0.0), span);
+    const double y = __fma_rn(a, K1, kMagic);
+    const uint32_t fq = (uint32_t)__double2loint(y);
+    const uint32_t ip = (uint32_t)__double2hiint(y) & 0x7FFFFu;
+    const uint32_t dh = (uint32_t)(draw >> 32);
+    uint32_t c = ip + (fq > dh ? 1u : 0u);
+    if ((fq - dh) <= 1u) c = exact_stoch_code_d(__dsub_rn(Tr::to_d(v[i]), lo), span, top, draw);
+    w |= (uint64_t)c << (i * BITS);
+  }
+  return w;
+}
+
 struct SeedOut {
-  U128 s0, inc;
+  U128 s0, inc;  // Philox stochastic (PH): s0 = the bucket's key (k0, k1)
   double r;
 };
 
-template <int INNER>
+template <int INNER, int PH = 0>
 __device__ __forceinline__ SeedOut seed_for(const QJobTable& tab, int64_t b, int S, double pitch) {
   SeedOut o;
   o.r = 0.0;
@@ -849,6 +871,10 @@ __device__ __forceinline__ SeedOut seed_for(const QJobTable& tab, int64_t b, int
   if (b < tab.total_buckets) {
     const BucketRef br = resolve_q(tab, b, S);
     const QJob& J = tab.jobs[br.j];
+    if (INNER == 1 && PH) {  // numpy Philox keyed like bucket_rng (generate_state(2))
+      philox_key(q_seed(tab, J), (uint64_t)(J.global_start + br.off), o.s0.lo, o.s0.hi);
+      return o;
+    }
     if (INNER == 0 && tab.noise == 1) {  // Philox: sample_shift's draw = word 0 of block 0
       uint64_t k0, k1;
       philox_key(q_seed(tab, J), (uint64_t)(J.global_start + br.off), k0, k1);
@@ -897,7 +923,10 @@ __device__ __forceinline__ BucketRef resolve_fast(const QJobTable& tab, int64_t 
   return r;
 }
 
-template <typename T, int INNER, int BITS, int NST, int FDQ = 0>
+// PH (INNER 1 only): numpy Philox4x64-10 noise -- a lane's octet draws words 0..3 of blocks
+// 2o and 2o+1 of the bucket's counter (no sequential stream, no jumps); octet buckets only
+// (the launcher keeps other shapes on the team kernels).
+template <typename T, int INNER, int BITS, int NST, int FDQ = 0, int PH = 0>
 __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_t* smem) {
   const int64_t poff = q_parity_off(tab);
   using Tr = InTraits<T>;
@@ -962,7 +991,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
   for (int64_t k = 0; bucket_of(k) < total; ++k) {
     if ((k & 31) == 0) {
       __syncwarp();
-      seeds[lane] = seed_for<INNER>(tab, bucket_of(k + lane), S, pitch);
+      seeds[lane] = seed_for<INNER, PH>(tab, bucket_of(k + lane), S, pitch);
       __syncwarp();
     }
     const int stage = (int)(k % NST);
@@ -1145,6 +1174,32 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
         }
       } else if (BITS != 16 && (S & 255) == 0) {
         if constexpr (BITS != 16) {
+        if constexpr (PH) {
+          const int ol = S / 256;
+          for (int g = 0; g < ol; ++g) {
+            const int o = g * 32 + lane;
+            T v[8];
+            lds_group(sb, 8 * o, v);
+            lds_group(sb, 8 * o + 4, v + 4);
+            const Philox4 b0 = philox_block((uint64_t)(2 * o), s0.lo, s0.hi);
+            const Philox4 b1 = philox_block((uint64_t)(2 * o + 1), s0.lo, s0.hi);
+            uint64_t w = 0;
+            bool unc = false;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              double a = __dsub_rn(Tr::to_d(v[i]), lo);
+              if constexpr (sizeof(T) == 8) a = fmin(fmax(a, 0.0), span);
+              const double y = __fma_rn(a, K1, kMagic);
+              const uint32_t fq = (uint32_t)__double2loint(y);
+              const uint32_t ip = (uint32_t)__double2hiint(y) & 0x7FFFFu;
+              const uint32_t dh = (uint32_t)((i < 4 ? b0.v[i] : b1.v[i - 4]) >> 32);
+              unc |= (fq - dh) <= 1u;
+              w |= (uint64_t)(ip + (fq > dh ? 1u : 0u)) << (i * BITS);
+            }
+            if (unc) w = philox_octet_exact<T, BITS>(sb + 8 * o, b0, b1, lo, span, K1, top);
+            store_octet<BITS>(cbase, o, w);
+          }
+        } else {
         // octets: lane owns 8 consecutive elements 8*o (o = lane, lane+32, ...), so the
         // stream jumps once per 8 draws (by 256-7) instead of once per 4.
         // jump constants from the (L1-resident) table, per bucket: keeps registers for the loop
@@ -1188,8 +1243,9 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
           }
           st = add128(mul128(OJa, st), jc);
         }
+        }  // PCG64
         }
-      } else {
+      } else if constexpr (!PH) {
         const JumpEntry e0 = g_jump[4 * lane + 1];
         U128 st = add128(mul128(e0.a, s0), mul128(e0.g, inc));  // state_{4*lane+1}
         const JumpEntry ej = g_jump[4 * 32 - 3];
@@ -1225,7 +1281,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
         }
       }
     } else if (n > 0) {
-      shift_f = quantize_bucket_general<T, INNER, BITS, FDQ>(q_seed(tab, J), (uint64_t)(J.global_start + br.off), in_smem ? sb : gx,
+      shift_f = quantize_bucket_general<T, INNER, BITS, FDQ, PH>(q_seed(tab, J), (uint64_t)(J.global_start + br.off), in_smem ? sb : gx,
                                                         n, gl, cbase, lof, hif, degenerate, lane, tab, J, br.off);
     }
     if (lane == 0) {
@@ -1241,10 +1297,10 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
   }
 }
 
-template <typename T, int INNER, int BITS, int NST, int FDQ = 0>
+template <typename T, int INNER, int BITS, int NST, int FDQ = 0, int PH = 0>
 __global__ void __launch_bounds__(256, 2) quantize_tma32_kernel(const __grid_constant__ QJobTable tab) {
   extern __shared__ __align__(128) uint8_t smem[];
-  quantize_tma32_body<T, INNER, BITS, NST, FDQ>(tab, smem);
+  quantize_tma32_body<T, INNER, BITS, NST, FDQ, PH>(tab, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -2082,7 +2138,7 @@ inline cudaError_t ensure_smem_attr(F kern, size_t smem, size_t (&cache)[64]) {
 }
 
 // Fast TMA path.  Returns false when the configuration needs the general kernel.
-template <typename T, int INNER, int BITS, int FDQ>
+template <typename T, int INNER, int BITS, int FDQ, int PH = 0>
 cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
   constexpr int NST = 2;
   const size_t stage = (size_t)tab.bucket * sizeof(T);
@@ -2098,7 +2154,7 @@ cudaError_t launch_q_tma32_v(const QJobTable& tab, int sms, cudaStream_t s) {
   const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t) +
                       (size_t)wpc * 32 * sizeof(SeedOut) + 33 * sizeof(JumpEntry) +
                       (dq_table_on(INNER, BITS, FDQ) ? (size_t)wpc * (1u << BITS) * sizeof(uint32_t) : 0);
-  auto kern = quantize_tma32_kernel<T, INNER, BITS, NST, FDQ>;
+  auto kern = quantize_tma32_kernel<T, INNER, BITS, NST, FDQ, PH>;
   static thread_local size_t smem_set[64] = {};  // per instantiation and device
   if (cudaError_t e = ensure_smem_attr(kern, smem, smem_set); e != cudaSuccess) return e;
   // tab.cta_cap (qsdp_comm_set_ctas_per_sm): leave CTA slots on every SM to a concurrent
@@ -2191,6 +2247,18 @@ cudaError_t launch_q_philox_tl(const QJobTable& tab, bool vec, int sms, cudaStre
 template <typename T, int INNER>
 cudaError_t launch_q_philox(const QJobTable& tab, bool vec, int sms, cudaStream_t s) {
   const int S = tab.bucket;
+  // K2 with octet buckets: the TMA32 quantizer with counter-based draws (no fused epilogue:
+  // the comm's push / fused paths are PCG64-only)
+  bool fdq = false;
+  for (int j = 0; j < tab.njobs; ++j) fdq = fdq || tab.jobs[j].dq_out != nullptr;
+  if (INNER == 1 && !fdq && S % 256 == 0 && S * (int)sizeof(T) <= 16384) {
+    switch (tab.bits) {
+      case 8: return launch_q_tma32_v<T, 1, 8, 0, 1>(tab, sms, s);
+      case 4: return launch_q_tma32_v<T, 1, 4, 0, 1>(tab, sms, s);
+      case 2: return launch_q_tma32_v<T, 1, 2, 0, 1>(tab, sms, s);
+      default: break;
+    }
+  }
   if (S % 8 != 0) {
     const int64_t blocks = (tab.total_buckets + 127) / 128;
     const int64_t cap = (int64_t)sms * 16;
