@@ -54,6 +54,25 @@ def main(path):
     print("by stream (ms):", {k: round(v * 1e-3, 2) for k, v in sorted(bystream.items(), key=lambda x: -x[1])})
     for k, v in sorted(byname.items(), key=lambda x: -x[1])[:15]:
         print(f"  {v * 1e-3:8.2f} ms  x{cnt[k]:5d}  {k}")
+    # host side: CUDA runtime calls by name, and the launches of each kernel category
+    corr = {e.get("args", {}).get("correlation"): cat(e["name"]) for e in ks}
+    rt = collections.defaultdict(float)
+    rtc = collections.Counter()
+    lc = collections.defaultdict(float)
+    lcc = collections.Counter()
+    for e in ev:
+        if e.get("ph") == "X" and e.get("cat") == "cuda_runtime":
+            rt[e["name"]] += e["dur"]
+            rtc[e["name"]] += 1
+            c = corr.get(e.get("args", {}).get("correlation"))
+            if c is not None and "aunch" in e["name"]:
+                lc[c] += e["dur"]
+                lcc[c] += 1
+    if rt:
+        print("CUDA runtime (ms, count):", {k: (round(v * 1e-3, 2), rtc[k]) for k, v in
+                                             sorted(rt.items(), key=lambda x: -x[1])[:8]})
+        print("launch time by kernel category (ms, count, us/launch):",
+              {k: (round(v * 1e-3, 2), lcc[k], round(v / max(lcc[k], 1), 1)) for k, v in lc.items()})
     # host side: user annotations (FSDP2's record_function ranges, optimizer, ...) by name
     ann = collections.defaultdict(float)
     acnt = collections.Counter()

@@ -36,9 +36,11 @@ def main():
     # (size, bucket, w bits, g bits, pad): pad 1 = shard_bounds, whose rank offsets are
     # not multiples of 4 for the odd sizes (the own-shard fused dequant must then
     # leave that shard to K3's scalar stores -- ADVICE r1)
+    # the last three are small collectives (a few buckets per rank, partial last buckets)
     cases = [(1 << 20, 1024, 8, 8, 1), (3 * 1024 * 1024 + 777, 1024, 8, 4, 1), (1000003, 1024, 8, 8, 1),
              (1 << 22, 1024, 8, 8, 1024), (50000, 64, 6, 4, 1),
-             (200000, 256, 4, 2, 256), (200000, 512, 16, 8, 1)]
+             (200000, 256, 4, 2, 256), (200000, 512, 16, 8, 1),
+             (4003, 1024, 8, 8, 1), (30011, 256, 4, 2, 1), (9000, 512, 16, 8, 1)]
     for size, bucket, wb, gb, pad in cases:
         segs = plan_segments(size, world, pad)
         maxseg = max(n for _, n in segs)
@@ -279,7 +281,13 @@ def missed_barrier(rank, world, dev):
 def philox_collectives(rank, world, dev):
     """C1/C2 with the counter-based noise (QSDP_NOISE_PHILOX4x64) at world > 1 (pull form)."""
     fails = 0
-    size, bucket = 500009, 1024
+    for size, bucket in ((500009, 1024), (20011, 1024)):  # the second: a small collective
+        fails += _philox_case(rank, world, dev, size, bucket)
+    return fails
+
+
+def _philox_case(rank, world, dev, size, bucket):
+    fails = 0
     segs = plan_segments(size, world, 1)
     ws, gs = QuantSpec(8, bucket, "shift", "philox"), QuantSpec(4, bucket, "uniform_stochastic", "philox")
     comm = QSDPComm(max(n for _, n in segs), ws, gs)
