@@ -38,6 +38,7 @@ not FSDP2's bf16 copy-in) and writes the dequantized weights as bf16
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 
@@ -97,10 +98,12 @@ class QSDPContext:
         self.rs = QSDPComm(max_shard_numel, wspec, gspec, group=group, device=device)
         # the comm streams overlap backward / forward compute: cap their SMs
         if sm_budget is None:
-            import os
             sm_budget = int(os.environ.get("QSDP_SM_BUDGET", "0"))
         self.ag.set_sm_budget(sm_budget)
         self.rs.set_sm_budget(sm_budget)
+        ag_ctas = int(os.environ.get("QSDP_AG_CTAS", "0"))  # all-gather quantizer CTAs per SM (0 = occupancy)
+        if ag_ctas:
+            self.ag.set_ctas_per_sm(ag_ctas)
         self.step = 0
         self.phase = PHASE_W_FWD
         self.calls = {"allgather": 0, "reducescatter": 0}
