@@ -320,7 +320,8 @@ typedef struct {
   int32_t raw;       /* non-zero: a full-precision piece (bias / norm, sharded.py:359-371, 414-429):
                         all-gather -- every rank's piece cast (RNE) to out_dtype; reduce-scatter --
                         out = (0.0 + v_0 + ... + v_{P-1}) / P in fp64, ranks in order, rounded once.
-                        Carried by the collective's barrier kernel (at most 48 per call). */
+                        Carried by the collective's barrier kernel (beyond 48 pieces, by a push
+                        kernel before it and a copy-out kernel after it). */
   int32_t reserved;
 } qsdp_piece;
 qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32_t npieces, int32_t in_dtype,

@@ -918,6 +918,19 @@ __global__ void __launch_bounds__(512) qsdp_barrier_raw_kernel(PeerFlags pf, uns
   if (t == 0 && world > 1) *reinterpret_cast<volatile unsigned long long*>(epoch_ptr) = target;
 }
 
+// Full-precision pieces beyond the barrier kernel's table (more than kMaxRaw in one call):
+// phase 0 pushes them before the barrier kernel (slot parity of the coming epoch, adj 1),
+// phase 1 copies out / averages them after it (the advanced epoch, adj 0).
+__global__ void __launch_bounds__(512) qsdp_raw_phase_kernel(const unsigned long long* epoch_ptr, int adj, int phase,
+                                                             RawTable rt) {
+  const int64_t par = rt.world > 1
+                          ? (int64_t)((*reinterpret_cast<const volatile unsigned long long*>(epoch_ptr) + (unsigned long long)adj) & 1ull) *
+                                rt.parity_stride
+                          : 0;
+  if (phase == 0) raw_push(rt, par);
+  else raw_post(rt, par);
+}
+
 __global__ void qsdp_counter_add_kernel(unsigned long long* p, unsigned long long delta) { *p += delta; }
 
 struct qsdp_comm {
@@ -1346,7 +1359,6 @@ static qsdp_status piece_layout(const qsdp_comm* c, const qsdp_qcfg* cfg, const 
     L.codes += round_up((size_t)qsdp_codes_bytes(pieces[k].numel, cfg), 16);
     L.meta += (size_t)qsdp_num_buckets(pieces[k].numel, cfg->bucket) * 12;
   }
-  if (L.nraw > kMaxRaw) return fail(QSDP_EINVAL, "more than 48 full-precision pieces in one group collective");
   for (int k = 0; k < np; ++k)
     if (pieces[k].raw && pieces[k].numel > 0) {
       L.code_off[k] = L.codes;
@@ -1381,11 +1393,26 @@ static qsdp_status pieces_barrier(qsdp_comm* c, const qsdp_piece* pieces, int32_
   rt.out = static_cast<uint8_t*>(out);
   rt.own_slots = c->slot(c->base, 0);
   for (int p = 0; p < c->world; ++p) rt.peer_slot[p] = c->slot(c->peer[p], c->rank);
-  for (int k = 0; k < np; ++k)
-    if (pieces[k].raw && pieces[k].numel > 0)
-      rt.p[rt.n++] = RawPieceDev{static_cast<const uint8_t*>(pieces[k].src), pieces[k].numel,
-                                 (int64_t)L.code_off[k], pieces[k].offset};
+  // the barrier kernel carries the first kMaxRaw pieces; any further ones go in tables of
+  // kMaxRaw through a push kernel before it and a copy-out / average kernel after it
+  std::vector<RawTable> extra;
+  for (int k = 0; k < np; ++k) {
+    if (!pieces[k].raw || pieces[k].numel <= 0) continue;
+    const RawPieceDev d{static_cast<const uint8_t*>(pieces[k].src), pieces[k].numel, (int64_t)L.code_off[k],
+                        pieces[k].offset};
+    if (rt.n < kMaxRaw) {
+      rt.p[rt.n++] = d;
+      continue;
+    }
+    if (extra.empty() || extra.back().n == kMaxRaw) {
+      extra.push_back(rt);
+      extra.back().n = 0;
+    }
+    extra.back().p[extra.back().n++] = d;
+  }
+  for (const RawTable& e : extra) qsdp_raw_phase_kernel<<<1, 512, 0, s>>>(c->epoch(), 1, 0, e);
   qsdp_barrier_raw_kernel<<<1, 512, 0, s>>>(pf, c->epoch(), c->err_dev, c->timeout_ns, rt);
+  for (const RawTable& e : extra) qsdp_raw_phase_kernel<<<1, 512, 0, s>>>(c->epoch(), 0, 1, e);
   QSDP_CUDA(cudaGetLastError());
   return QSDP_OK;
 }

@@ -331,6 +331,10 @@ def group_pieces(rank, world, dev):
         off += n
         roffs.append(off)
         off += r
+    for k in range(56):  # 60 full-precision pieces: more than the barrier kernel's table of 48
+        raw_sizes.append(1 + k % 5)
+        roffs.append(off)
+        off += raw_sizes[-1]
     stride = off
     cap = sum(sizes) + len(sizes) * (1024 + 16) + 4 * (sum(raw_sizes) + 4 * len(raw_sizes))
     comm = QSDPComm(cap, QuantSpec(8, 1024, "shift"), QuantSpec(8, 1024, "uniform_stochastic"))
