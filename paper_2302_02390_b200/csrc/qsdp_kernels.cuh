@@ -1230,7 +1230,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             const uint32_t dh = pcg_output_hi32(st);
             unc |= (fq - dh) <= 1u;  // the only uncertain case
             w |= (uint64_t)(ip + (fq > dh ? 1u : 0u)) << (i * BITS);
-            if (i < 7) st = pcg_step(st, inc);
+            if (i < 7) st = FDQ == 0 ? add128_cc(mul128(st, pcg_mult()), inc) : pcg_step(st, inc);
           }
           if (unc) w = stoch_octet_exact<T, BITS>(sb + 8 * o, st0, inc, lo, span, K1, top);
           if (!FDQ || !tab.dq_nocodes) store_octet<BITS>(cbase, o, w);
@@ -1241,7 +1241,7 @@ __device__ __forceinline__ void quantize_tma32_body(const QJobTable& tab, uint8_
             dq_emit4<BITS, FDQ>(fqs, 8 * o, 4, w);
             dq_emit4<BITS, FDQ>(fqs, 8 * o + 4, 4, w >> (4 * BITS));
           }
-          st = add128(mul128(OJa, st), jc);
+          st = FDQ == 0 ? add128_cc(mul128(OJa, st), jc) : add128(mul128(OJa, st), jc);
         }
         }  // PCG64
         }
