@@ -86,6 +86,9 @@ def parse():
                          "steady state (N=1 +2%%, DESIGN §17)")
     ap.add_argument("--bwd-ag-ctas", type=int, default=1, help="quantizer CTAs per SM, backward all-gathers")
     ap.add_argument("--rs-ctas", type=int, default=0, help="quantizer CTAs per SM, reduce-scatters")
+    ap.add_argument("--rs-priority", type=int, default=0,
+                    help="CUDA stream priority of the reduce-scatter streams (-1 = high: their CTAs are "
+                         "dispatched before queued all-gather CTAs)")
     ap.add_argument("--trace", default="", help="write the GPU timeline of one step replay (CUPTI via "
                     "torch.profiler: every kernel's start / end / stream) and its overlap summary to this JSON file")
     ap.add_argument("--gpt-steps", type=int, default=8)
@@ -391,7 +394,7 @@ def main():
     comm, rs_comm = ag_comms[0], rs_comms[0]
     # all-gather slot 0 runs on the issuing stream (the capture stream inside a graph)
     ag_side = [torch.cuda.Stream(device=dev) for _ in range(K - 1)]
-    rs_side = [torch.cuda.Stream(device=dev) for _ in range(K)]
+    rs_side = [torch.cuda.Stream(device=dev, priority=args.rs_priority) for _ in range(K)]
     rs_stream = rs_side[0]
 
     # ---- the step as a list of launches (kind, bytes, fn) ----
