@@ -16,6 +16,7 @@
 // the barrier of call k+1, i.e. finished reading call k-1's data.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdint>
@@ -56,6 +57,13 @@ cudaError_t launch_unpack_codes(const uint8_t* packed, int64_t length, int bucke
 }  // namespace qsdp
 
 using namespace qsdp;
+
+// NVTX range over one C-ABI call (host side: the enqueue of its launches), so an nsys / ncu
+// timeline (ncu --nvtx) attributes the kernels to the collective that issued them.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace {
 
@@ -346,6 +354,7 @@ void qsdp_shard_bounds(int64_t size, int32_t world, qsdp_segment* out) {
 
 qsdp_status qsdp_quantize(const void* x, int32_t x_dtype, qsdp_segment seg, const qsdp_qcfg* cfg,
                           const qsdp_key* key, uint8_t* codes, float* meta, uint64_t* d_bad, void* stream) {
+  NvtxRange nvtx_("qsdp_quantize");
   qsdp_qitem it;
   it.x = x;
   it.seg = seg;
@@ -357,6 +366,7 @@ qsdp_status qsdp_quantize(const void* x, int32_t x_dtype, qsdp_segment seg, cons
 
 qsdp_status qsdp_quantize_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
                                 const qsdp_qcfg* cfg, uint64_t* d_bad, void* stream) {
+  NvtxRange nvtx_("qsdp_quantize_batch");
   return qsdp_quantize_batch_dstep(items, nitems, x_dtype, cfg, d_bad, nullptr, stream);
 }
 
@@ -398,6 +408,7 @@ static qsdp_status quantize_items(const qsdp_qitem* items, int32_t nitems, int32
 qsdp_status qsdp_quantize_batch_dstep(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
                                       const qsdp_qcfg* cfg, uint64_t* d_bad, const uint64_t* d_step,
                                       void* stream) {
+  NvtxRange nvtx_("qsdp_quantize_batch_dstep");
   return quantize_items(items, nitems, x_dtype, cfg, d_bad, d_step, nullptr, 0, stream);
 }
 
@@ -419,6 +430,7 @@ qsdp_status qsdp_levels_stochastic(const double* d_values, int64_t n, const doub
 qsdp_status qsdp_quantize_stream(const void* x, int32_t x_dtype, int64_t length, const qsdp_qcfg* cfg,
                                  const uint64_t* d_states, uint8_t* codes, float* meta, uint32_t* d_scratch,
                                  void* stream) {
+  NvtxRange nvtx_("qsdp_quantize_stream");
   qsdp_status st = check_cfg(cfg);
   if (st != QSDP_OK) return st;
   if (cfg->noise != QSDP_NOISE_PCG64_SEEDSEQ) return fail(QSDP_EINVAL, "a shared stream replays numpy PCG64");
@@ -439,6 +451,7 @@ qsdp_status qsdp_quantize_stream(const void* x, int32_t x_dtype, int64_t length,
 qsdp_status qsdp_quantize_levels_batch(const qsdp_qitem* items, int32_t nitems, int32_t x_dtype,
                                        const qsdp_qcfg* cfg, const double* d_levels, int32_t nlevels,
                                        uint64_t* d_bad, void* stream) {
+  NvtxRange nvtx_("qsdp_quantize_levels_batch");
   if (d_levels == nullptr) return fail(QSDP_EINVAL, "inner 'levels' requires a LevelTable");
   if (!pow2(nlevels)) return fail(QSDP_EINVAL, "level count must be a power of two");
   if (cfg != nullptr && cfg->bits >= 1 && cfg->bits <= 16 && nlevels > (1 << cfg->bits))
@@ -460,6 +473,7 @@ qsdp_status qsdp_quantize_levels(const void* x, int32_t x_dtype, int64_t length,
 
 qsdp_status qsdp_dequantize(const uint8_t* codes, const float* meta, int64_t length, const qsdp_qcfg* cfg,
                             void* out, int32_t out_dtype, void* stream) {
+  NvtxRange nvtx_("qsdp_dequantize");
   qsdp_ditem it;
   memset(&it, 0, sizeof(it));
   it.codes[0] = codes;
@@ -498,6 +512,7 @@ static qsdp_status dequant_items(const qsdp_ditem* items, int32_t nitems, const 
 qsdp_status qsdp_dequantize_levels_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
                                          const double* d_levels, int32_t nlevels, int32_t out_dtype,
                                          void* stream) {
+  NvtxRange nvtx_("qsdp_dequantize_levels_batch");
   if (d_levels == nullptr) return fail(QSDP_EINVAL, "mode 'levels' requires a LevelTable");
   if (cfg != nullptr && (cfg->bits < 1 || cfg->bits > 16 || nlevels != (1 << cfg->bits)))
     return fail(QSDP_EINVAL, "level table size does not match bit_width");
@@ -531,12 +546,14 @@ qsdp_status qsdp_learn_levels(const double* d_values, int64_t n, double* d_level
 
 qsdp_status qsdp_dequantize_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
                                   int32_t out_dtype, void* stream) {
+  NvtxRange nvtx_("qsdp_dequantize_batch");
   return dequant_items(items, nitems, cfg, 0, 1, out_dtype, stream);
 }
 
 qsdp_status qsdp_dequant_accumulate(const uint8_t* const* codes, const float* const* meta, int32_t nsrc,
                                     int64_t length, const qsdp_qcfg* cfg, int32_t divisor, void* out,
                                     int32_t out_dtype, void* stream) {
+  NvtxRange nvtx_("qsdp_dequant_accumulate");
   if (nsrc < 1 || nsrc > 8) return fail(QSDP_EINVAL, "nsrc must be in [1, 8]");
   qsdp_ditem it;
   memset(&it, 0, sizeof(it));
@@ -552,6 +569,7 @@ qsdp_status qsdp_dequant_accumulate(const uint8_t* const* codes, const float* co
 
 qsdp_status qsdp_dequant_accumulate_batch(const qsdp_ditem* items, int32_t nitems, const qsdp_qcfg* cfg,
                                           int32_t divisor, int32_t out_dtype, void* stream) {
+  NvtxRange nvtx_("qsdp_dequant_accumulate_batch");
   return dequant_items(items, nitems, cfg, 1, divisor, out_dtype, stream);
 }
 
@@ -1200,6 +1218,7 @@ static bool fdq_ok(const qsdp_qcfg* cfg, int in_dtype, int out_dtype) {
 
 qsdp_status qsdp_all_gather(qsdp_comm* c, const void* shard, int32_t in_dtype, const qsdp_segment* segs,
                             const qsdp_key* key, void* full_out, int32_t out_dtype, void* stream) {
+  NvtxRange nvtx_("qsdp_all_gather");
   if (c == nullptr || key == nullptr) return fail(QSDP_EINVAL, "null argument");
   qsdp_status st = comm_failed(c);
   if (st != QSDP_OK) return st;
@@ -1266,6 +1285,7 @@ static qsdp_status reduce_scatter_impl(qsdp_comm* c, const void* full_grad, int3
 
 qsdp_status qsdp_reduce_scatter(qsdp_comm* c, const void* full_grad, int32_t in_dtype, const qsdp_segment* segs,
                                 const qsdp_key* key, void* shard_out, int32_t out_dtype, void* stream) {
+  NvtxRange nvtx_("qsdp_reduce_scatter");
   if (shard_out == nullptr) return fail(QSDP_EINVAL, "null output");
   return reduce_scatter_impl(c, full_grad, in_dtype, segs, key, shard_out, out_dtype, stream, nullptr, nullptr);
 }
@@ -1420,6 +1440,7 @@ static qsdp_status pieces_barrier(qsdp_comm* c, const qsdp_piece* pieces, int32_
 qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32_t npieces, int32_t in_dtype,
                                    int64_t rank_stride, const qsdp_key* key, void* full_out, int32_t out_dtype,
                                    void* stream) {
+  NvtxRange nvtx_("qsdp_all_gather_pieces");
   if (c == nullptr || key == nullptr || full_out == nullptr) return fail(QSDP_EINVAL, "null argument");
   qsdp_status st = comm_failed(c);
   if (st != QSDP_OK) return st;
@@ -1486,6 +1507,7 @@ qsdp_status qsdp_all_gather_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32
 qsdp_status qsdp_reduce_scatter_pieces(qsdp_comm* c, const qsdp_piece* pieces, int32_t npieces, int32_t in_dtype,
                                        int64_t rank_stride, const qsdp_key* key, void* shard_out, int32_t out_dtype,
                                        void* stream) {
+  NvtxRange nvtx_("qsdp_reduce_scatter_pieces");
   if (c == nullptr || key == nullptr || shard_out == nullptr) return fail(QSDP_EINVAL, "null argument");
   qsdp_status st = comm_failed(c);
   if (st != QSDP_OK) return st;
@@ -1546,6 +1568,7 @@ qsdp_status qsdp_reduce_scatter_pieces(qsdp_comm* c, const qsdp_piece* pieces, i
 qsdp_status qsdp_reduce_scatter_lattice(qsdp_comm* c, const void* full_grad, int32_t in_dtype, const qsdp_segment* segs,
                                         const qsdp_key* key, void* shard_out, int32_t out_dtype, void* x_shard,
                                         const qsdp_lattice* lat, void* stream) {
+  NvtxRange nvtx_("qsdp_reduce_scatter_lattice");
   qsdp_status st = check_lattice(lat, x_shard);
   if (st != QSDP_OK) return st;
   return reduce_scatter_impl(c, full_grad, in_dtype, segs, key, shard_out, out_dtype, stream, x_shard, lat);
