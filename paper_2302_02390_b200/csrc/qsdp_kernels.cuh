@@ -348,6 +348,31 @@ struct Coder {
     }
   }
 
+  // Bucket setup from a lane-parallel seed (seed_for): the same scales and noise as setup()
+  // (PCG64 only) without every lane of the team re-running SeedSequence.
+  template <typename SO>
+  __device__ __forceinline__ void setup_seeded(float lof, float hif, int bits, const SO& sd, int lt, int TL,
+                                               float& shift_f) {
+    top = (double)((1u << bits) - 1u);
+    lo = (double)lof;
+    span = __dsub_rn((double)hif, lo);
+    inv = __drcp_rn(span);
+    pitch = __ddiv_rn(1.0, top);
+    r = 0.0;
+    if (INNER == 0) {
+      r = sd.r;
+      shift_f = __double2float_rn(__dmul_rn(r, span));  // _f32(r*(hi-lo))
+      return;
+    }
+    inc = sd.inc;
+    const JumpEntry e0 = g_jump[4 * lt + 1];
+    st = add128(mul128(e0.a, sd.s0), mul128(e0.g, inc));
+    const JumpEntry ej = g_jump[4 * TL - 3];
+    jmp_a = ej.a;
+    jmp_c = mul128(ej.g, inc);
+    shift_f = 0.0f;
+  }
+
   __device__ __forceinline__ void step() { st = pcg_step(st, inc); }
   __device__ __forceinline__ void jump() { st = add128(mul128(jmp_a, st), jmp_c); }
 
@@ -450,6 +475,42 @@ __device__ __forceinline__ BucketRef resolve_q(const QJobTable& tab, int64_t b, 
   return r;
 }
 
+struct SeedOut {
+  U128 s0, inc;  // Philox stochastic (PH): s0 = the bucket's key (k0, k1)
+  double r;
+};
+
+template <int INNER, int PH = 0>
+__device__ __forceinline__ SeedOut seed_for(const QJobTable& tab, int64_t b, int S, double pitch) {
+  SeedOut o;
+  o.r = 0.0;
+  o.s0 = U128{0, 0};
+  o.inc = U128{0, 0};
+  if (b < tab.total_buckets) {
+    const BucketRef br = resolve_q(tab, b, S);
+    const QJob& J = tab.jobs[br.j];
+    if (INNER == 1 && PH) {  // numpy Philox keyed like bucket_rng (generate_state(2))
+      philox_key(q_seed(tab, J), (uint64_t)(J.global_start + br.off), o.s0.lo, o.s0.hi);
+      return o;
+    }
+    if (INNER == 0 && tab.noise == 1) {  // Philox: sample_shift's draw = word 0 of block 0
+      uint64_t k0, k1;
+      philox_key(q_seed(tab, J), (uint64_t)(J.global_start + br.off), k0, k1);
+      const double d = u64_to_unit_double(philox_block(0, k0, k1).v[0]);
+      o.r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));
+      return o;
+    }
+    seed_bucket(q_seed(tab, J), (uint64_t)(J.global_start + br.off), o.s0, o.inc);
+    if (INNER == 0) {
+      const U128 s1 = mad128(o.s0, pcg_mult(), o.inc);
+      const double d = u64_to_unit_double(pcg_output(s1));
+      o.r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));  // uniform(-p/2, p/2)
+    }
+  }
+  return o;
+}
+
+
 // ---------------------------------------------------------------------------
 // K1/K2 fast path: TMA-pipelined quantizer for the direct widths.
 // Requirements (host-checked): BITS in {2,4,8,16}, S % 8 == 0, S*sizeof(T) <= 8 KB (16 KB for the TMA32 kernel).
@@ -469,6 +530,12 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
   const int64_t stage_elems = (int64_t)TEAMS * S;
   T* wbuf = reinterpret_cast<T*>(smem) + (int64_t)wib * NST * stage_elems;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)wpc * NST * stage_elems * sizeof(T)) + wib * NST;
+  // seeds of the warp's next 32 buckets (32 / TEAMS iterations), one lane each: SeedSequence runs
+  // once per bucket instead of once per team lane (a 64-element bucket is 16 lanes x 4 elements)
+  SeedOut* seeds = reinterpret_cast<SeedOut*>(smem + (size_t)wpc * NST * stage_elems * sizeof(T) +
+                                              (size_t)wpc * NST * sizeof(uint64_t)) + wib * 32;
+  constexpr int ITS = 32 / TEAMS;  // iterations per seed batch
+  const double seed_pitch = __ddiv_rn(1.0, (double)((1u << BITS) - 1u));
   const int64_t gw = (int64_t)blockIdx.x * wpc + wib;
   const int64_t nw = (int64_t)gridDim.x * wpc;
   const int64_t total = tab.total_buckets;
@@ -507,6 +574,11 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
     if ((gw + k * nw) * TEAMS < total) issue(k);
 
   for (int64_t k = 0; (gw + k * nw) * TEAMS < total; ++k) {
+    if (k % ITS == 0) {
+      __syncwarp();
+      seeds[lane] = seed_for<INNER>(tab, (gw + (k + lane / TEAMS) * nw) * TEAMS + lane % TEAMS, S, seed_pitch);
+      __syncwarp();
+    }
     const int stage = (int)(k % NST);
     mbar_wait(&bars[stage], (uint32_t)((k / NST) & 1));
     const T* sb = wbuf + stage * stage_elems + (int64_t)team * S;
@@ -566,8 +638,7 @@ __global__ void __launch_bounds__(256) quantize_tma_kernel(const __grid_constant
     // ---- pass 2: codes ----------------------------------------------------------
     Coder<T, INNER> cd;
     float shift_f = 0.0f;
-    if (active && !degenerate)
-      cd.setup(lof, hif, BITS, q_seed(tab, J), (uint64_t)(J.global_start + br.off), lt, TL, shift_f, tab.noise);
+    if (active && !degenerate) cd.setup_seeded(lof, hif, BITS, seeds[(k % ITS) * TEAMS + team], lt, TL, shift_f);
     uint8_t* cbase = J.codes + poff + br.lb * pbs;
     const int64_t pb = payload_bytes(n, BITS);
     if (active && !degenerate && in_smem) {
@@ -855,41 +926,6 @@ static __device__ __noinline__ uint64_t philox_octet_exact(const T* v, Philox4 b
     w |= (uint64_t)c << (i * BITS);
   }
   return w;
-}
-
-struct SeedOut {
-  U128 s0, inc;  // Philox stochastic (PH): s0 = the bucket's key (k0, k1)
-  double r;
-};
-
-template <int INNER, int PH = 0>
-__device__ __forceinline__ SeedOut seed_for(const QJobTable& tab, int64_t b, int S, double pitch) {
-  SeedOut o;
-  o.r = 0.0;
-  o.s0 = U128{0, 0};
-  o.inc = U128{0, 0};
-  if (b < tab.total_buckets) {
-    const BucketRef br = resolve_q(tab, b, S);
-    const QJob& J = tab.jobs[br.j];
-    if (INNER == 1 && PH) {  // numpy Philox keyed like bucket_rng (generate_state(2))
-      philox_key(q_seed(tab, J), (uint64_t)(J.global_start + br.off), o.s0.lo, o.s0.hi);
-      return o;
-    }
-    if (INNER == 0 && tab.noise == 1) {  // Philox: sample_shift's draw = word 0 of block 0
-      uint64_t k0, k1;
-      philox_key(q_seed(tab, J), (uint64_t)(J.global_start + br.off), k0, k1);
-      const double d = u64_to_unit_double(philox_block(0, k0, k1).v[0]);
-      o.r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));
-      return o;
-    }
-    seed_bucket(q_seed(tab, J), (uint64_t)(J.global_start + br.off), o.s0, o.inc);
-    if (INNER == 0) {
-      const U128 s1 = mad128(o.s0, pcg_mult(), o.inc);
-      const double d = u64_to_unit_double(pcg_output(s1));
-      o.r = __dadd_rn(__dmul_rn(pitch, -0.5), __dmul_rn(pitch, d));  // uniform(-p/2, p/2)
-    }
-  }
-  return o;
 }
 
 __device__ __forceinline__ U128 shfl_u128(const U128& v, int src) {
@@ -2186,7 +2222,8 @@ cudaError_t launch_q_tma(const QJobTable& tab, bool vec, int sms, cudaStream_t s
     const size_t stage = (size_t)TEAMS * tab.bucket * sizeof(T);
     int wpc = 8;
     while (wpc > 1 && (size_t)wpc * NST * stage > 64 * 1024) wpc >>= 1;
-    const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t);
+    const size_t smem = (size_t)wpc * NST * stage + (size_t)wpc * NST * sizeof(uint64_t) +
+                        (size_t)wpc * 32 * sizeof(SeedOut);
     auto kern = quantize_tma_kernel<T, INNER, BITS, TL, NST>;
     static thread_local size_t smem_set[64] = {};
     if (cudaError_t e = ensure_smem_attr(kern, smem, smem_set); e != cudaSuccess) return e;
