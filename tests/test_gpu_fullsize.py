@@ -73,3 +73,30 @@ def test_gpt2_small_step_properties_and_sampled_parity(oracle):
                 exp = oracle.dequantize_segment(c, m, e - a, S, BITS, 1).astype(np.float32)
                 assert np.array_equal(ys[a:e], exp), (gi, kind, b)
     comm.close()
+
+
+def test_two_gigabyte_tensor_sampled_parity(oracle):
+    """A 2^29 + 1000-element (2 GB fp32) tensor -- past the top of the SURVEY §8(d) sweep --
+    through one all-gather / reduce-scatter: input byte offsets past 2^31 (64-bit indexing
+    everywhere), checked on sampled buckets across the whole range, the last ones included."""
+    dev = torch.device("cuda", 0)
+    n = (1 << 29) + 1000
+    gen = torch.Generator(device=dev).manual_seed(7)
+    comm = QSDPComm(n, QuantSpec(BITS, S, "shift"), QuantSpec(4, S, "uniform_stochastic"), device=dev)
+    x = torch.randn(n, generator=gen, device=dev) * 0.02
+    out = torch.empty(n, device=dev)
+    comm.all_gather(x, [(0, n)], SegmentKey(1, 9, 2, 1, 0), out)
+    sh = torch.empty(n, device=dev)
+    comm.reduce_scatter(x, [(0, n)], SegmentKey(1, 9, 2, 2, 0), sh)
+    torch.cuda.synchronize()
+    nb = (n + S - 1) // S
+    rng = np.random.default_rng(3)
+    picks = sorted(set(rng.choice(nb, size=48, replace=False).tolist()) | {0, nb // 2, nb - 2, nb - 1})
+    for b in picks:
+        a, e = b * S, min(n, (b + 1) * S)
+        xs = x[a:e].cpu().numpy()
+        for inner, bits, phase, y in ((0, BITS, 1, out), (1, 4, 2, sh)):
+            c, m, _ = oracle.quantize_segment(xs, a, S, bits, inner, (1, 9, 2, phase, 0), 1)
+            exp = oracle.dequantize_segment(c, m, e - a, S, bits, 1).astype(np.float32)
+            assert np.array_equal(y[a:e].cpu().numpy(), exp), (b, inner)
+    comm.close()
