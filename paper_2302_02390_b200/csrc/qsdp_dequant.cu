@@ -36,7 +36,10 @@ static cudaError_t launch_d_tl(const DJobTable& tab, bool vec, int sms, cudaStre
 
 template <int BITS, int OUT, bool ACC>
 static cudaError_t launch_d_bits(const DJobTable& tab, bool vec, int sms, cudaStream_t s) {
-  const int tl = team_lanes(tab.bucket);
+  int tl = team_lanes(tab.bucket);
+  // small buckets (S <= 64): narrower teams -- more buckets per warp iteration share the
+  // per-bucket work (job lookup, scales) and each lane keeps several groups' loads in flight
+  if (tl == 16) tl = ACC ? 8 : 4;
   if constexpr (ACC) {  // per-source scale rows are filled by lanes 0..nsrc-1: teams of >= 8 lanes
     if (tl <= 8) return launch_d_tl<BITS, 8, OUT, ACC>(tab, vec, sms, s);
     if (tl == 16) return launch_d_tl<BITS, 16, OUT, ACC>(tab, vec, sms, s);

@@ -2320,7 +2320,12 @@ cudaError_t launch_q_t(const QJobTable& tab, bool vec, int sms, cudaStream_t s) 
     quantize_generic_kernel<T, INNER><<<(int)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks)), 128, 0, s>>>(tab);
     return cudaGetLastError();
   }
-  switch (team_lanes(S)) {
+  int tl = team_lanes(S);
+  const bool direct = tab.bits == 2 || tab.bits == 4 || tab.bits == 8 || tab.bits == 16;
+  // S in (32, 64], whole-byte groups: 8 buckets per warp, 4 groups per lane (the per-bucket work
+  // is shared by more buckets per warp instruction; odd widths keep their lane-pair packing)
+  if (tl == 16 && direct) tl = 4;
+  switch (tl) {
     case 2: return launch_q_tl<T, INNER, 2>(tab, vec, sms, s);
     case 4: return launch_q_tl<T, INNER, 4>(tab, vec, sms, s);
     case 8: return launch_q_tl<T, INNER, 8>(tab, vec, sms, s);
